@@ -1,0 +1,137 @@
+"""Pin the CPU oracle (oracle/) against the reference's own outputs.
+
+The fixtures in tests/golden/reference_golden.json were produced by running
+the unmodified reference package (tests/golden/make_golden.py).  Every oracle
+function is checked against them here; only then is the oracle trusted as the
+checker for the CUDA path (tests/test_gpu_parity.py).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2310_19373_b200 import instances as I
+
+
+def _coeffs(case):
+    return np.array(case["coeffs"], dtype=np.float64)
+
+
+def test_splitmix64_known_answers(golden):
+    # instances.py:28-29 and test_instances.py:19-29 of the reference
+    assert golden["splitmix64"]["1234567"][:3] == [6457827717110365317, 3203168211198807973, 9817491932198370423]
+    assert golden["splitmix64"]["0"][0] == 16294208416658607535
+    for seed, outs in golden["splitmix64"].items():
+        r = I.SplitMix64(int(seed))
+        assert [r.next_u64() for _ in outs] == outs
+        assert [int(v) for v in I._u64_stream(int(seed), len(outs))] == outs
+
+
+def test_bench_seed(golden):
+    for key, want in golden["bench_seed"].items():
+        n, rep = map(int, key.split(","))
+        assert I.bench_seed(n, rep) == want
+
+
+def test_random_instance_bit_exact(golden):
+    for key, want in golden["random_instance_sha256"].items():
+        n, seed, d = key.split(",")
+        assert I.coeffs_sha256(I.random_instance(int(n), int(seed), float(d)).coeffs) == want, key
+
+
+def test_config_generators_pinned(golden):
+    by_name = {c["name"]: c for c in golden["cases"]}
+    for rep in range(3):
+        assert I.coeffs_sha256(I.config_coeffs("A", rep)) == by_name[f"configA_n20_rep{rep}"]["sha256"]
+    assert I.coeffs_sha256(I.config_coeffs("B", 0)) == by_name["configB_n24_rep0"]["sha256"]
+    assert I.coeffs_sha256(I.config_coeffs("D", 0)) == by_name["configD_n32_rep0"]["sha256"]
+    for rep in range(2):
+        assert I.coeffs_sha256(I.config_coeffs("E", rep, n=22)) == by_name[f"configE_n22_rep{rep}"]["sha256"]
+
+
+def test_eval_upper_worked_example():
+    # test_core.py:88-95 of the reference
+    c = np.array([[1.0, -2.0, 0.0], [0.0, 3.0, 1.0], [0.0, 0.0, -1.0]])
+    assert O.eval_upper(c, [1.0, 1.0, 0.0]) == 2.0
+
+
+def test_gray_scan_matches_reference_kernel(golden):
+    for case in golden["gray_scan"]:
+        c = np.array(case["coeffs"])
+        qua, lin = O.split(c)
+        xm, vm, steps = O.gray_scan(c, qua, lin, np.array(case["x0"]), case["v0"], case["n_free"])
+        assert xm.tolist() == case["x_min"]
+        assert vm == case["v_min"]
+        assert steps == case["steps"]
+
+
+def _check_case(case, skip_big=True):
+    c = _coeffs(case)
+    n = case["n"]
+    res = case["results"]
+    if "incremental" in res:
+        bits, val, ev = O.solve_incremental(c)
+        assert (bits, val, ev) == (res["incremental"]["bits"], res["incremental"]["value"],
+                                   res["incremental"]["evaluations"]), case["name"]
+    for key, want in res.items():
+        if key.startswith("parallel_m"):
+            m = int(key[len("parallel_m"):])
+            if skip_big and n >= 30:
+                continue
+            bits, val, ev = O.solve_subspaces(c, m, threads=4)
+            assert (bits, val, ev) == (want["bits"], want["value"], want["evaluations"]), (case["name"], key)
+        elif key == "naive":
+            xm, v, steps = O.naive_scan(c)
+            bits = int(sum(int(b) << i for i, b in enumerate(xm)))
+            assert bits == want["bits"] and steps == want["evaluations"], case["name"]
+            assert O.eval_upper(c, xm) == want["value"]
+        elif key.startswith("subspace_m"):
+            m = int(key[len("subspace_m"):])
+            for s, w in enumerate(want):
+                bits, val, ev = O.solve_subspaces(c, m, s, s + 1)
+                assert (bits, val, ev) == (w["bits"], w["value"], w["evaluations"]), (case["name"], key, s)
+
+
+def test_oracle_solvers_match_reference(golden):
+    for case in golden["cases"]:
+        _check_case(case)
+
+
+@pytest.mark.slow
+def test_oracle_config_d_full(golden):
+    case = next(c for c in golden["cases"] if c["name"] == "configD_n32_rep0")
+    _check_case(case, skip_big=False)
+
+
+def test_tie_rules_certified_by_enumeration(golden):
+    """The tie rules the GPU path implements reproduce every
+    reference choice: lowest global Gray rank (incremental), lowest
+    (suffix, local Gray rank) (parallel m / subspace), lowest integer (naive)."""
+    for case in golden["cases"]:
+        n = case["n"]
+        if n > 20:
+            continue
+        c = _coeffs(case)
+        res = case["results"]
+        if "incremental" in res:
+            bits, val, _ = O.expected_argmin(c, 0)
+            assert bits == res["incremental"]["bits"], case["name"]
+        for key, want in res.items():
+            if key.startswith("parallel_m"):
+                m = int(key[len("parallel_m"):])
+                assert O.expected_argmin(c, m)[0] == want["bits"], (case["name"], key)
+            elif key == "naive":
+                assert O.expected_argmin(c, 0, rule="integer")[0] == want["bits"], case["name"]
+            elif key.startswith("subspace_m"):
+                m = int(key[len("subspace_m"):])
+                for s, w in enumerate(want):
+                    assert O.expected_argmin(c, m, suffix=s)[0] == w["bits"], (case["name"], key, s)
+
+
+def test_config_c_batch(golden):
+    cb = golden["configC"]
+    batch = I.config_batch(cb["count"], cb["n"])
+    assert I.coeffs_sha256(batch) == cb["sha256"]
+    bits, vals = O.solve_batch(batch, threads=8)
+    assert [int(b) for b in bits] == cb["bits"]
+    assert vals.tolist() == cb["values"]
