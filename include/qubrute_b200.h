@@ -1,0 +1,117 @@
+/*
+ * qubrute_b200 — B200-native (sm_100a) Gray-code brute-force QUBO solver.
+ *
+ * C ABI of libqubrute_b200.so.  Plain pointers and sizes only; the caller owns
+ * every buffer, the library never retains a caller pointer after returning,
+ * device memory / streams are library-owned and persistent per device after
+ * qb_init().  Every entry point is safe to call from several host threads
+ * (calls on one device are serialised by a per-device mutex); loaded through
+ * ctypes.CDLL the GIL is released for the duration of a call.
+ *
+ * Status codes: QB_OK (0) on success, a negative QB_E_* otherwise; the message
+ * is available from qb_last_error() (thread-local).  Argument validation that
+ * the reference performs in Python (dimension cap, fixed-bit range, suffix
+ * range) is repeated here and reported as QB_E_ARG / QB_E_CAP.
+ *
+ * The reference ("qubrute", arXiv 2310.19373) has no native interface: its hot
+ * path is the numba kernel _kernels.gray_scan reached from solver.py.  The
+ * functions below are what a binding of that path needs; each cites the
+ * reference interface it replaces.  INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef QUBRUTE_B200_H
+#define QUBRUTE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QB_OK 0
+#define QB_E_ARG (-1)      /* invalid argument (reference raises ValueError) */
+#define QB_E_CAP (-2)      /* n above QB_MAX_DIM (reference raises DimensionCapError) */
+#define QB_E_CUDA (-3)     /* CUDA runtime error */
+#define QB_E_NODEV (-4)    /* no CUDA device / library not initialised on one */
+#define QB_E_INTERNAL (-5) /* invariant violated (reported, never silently ignored) */
+
+#define QB_MAX_DIM 40      /* reference core.py:24 MAX_DIM */
+
+/* Tie rules (which of several exact minimisers is returned). */
+#define QB_TIE_GRAY 0      /* lowest (suffix, Gray rank of free bits): solve_incremental (m_tie=0),
+                              solve_parallel(fixed_bits=m_tie), solve_subspace -- solver.py:118-229 */
+#define QB_TIE_INTEGER 1   /* lowest integer encoding: solve_naive -- solver.py:99-115, _kernels.py:23-43 */
+
+/* Traversal kernel variants. */
+#define QB_VARIANT_AUTO 0      /* table kernel (fastest exact path) */
+#define QB_VARIANT_TABLE 1     /* blocked Gray walk: outer field updates + inner-block table */
+#define QB_VARIANT_FIELDWALK 2 /* per-step Gray walk with register local fields (Alg. 1 form) */
+
+/* Result of one solve (or of one shard of a sharded solve). */
+typedef struct qb_result {
+  uint64_t argmin_bits;   /* minimiser, bit i = x_i (reference Solution.minimizer, core.py:153-162) */
+  double value;           /* eval_upper(minimiser) in the reference's fp64 order (solver.py:169) */
+  uint64_t tie_key;       /* position of the minimiser under the tie rule (lower wins) */
+  uint64_t value_key;     /* order-preserving 64-bit image of the compared value (lower wins);
+                             combine shards by lexicographic min of (value_key, tie_key) */
+  uint64_t states;        /* states scanned by this call */
+  int32_t exact;          /* 1: values compared exactly (integer-exact path), 0: certified
+                             filter + exact re-evaluation of near-minimal candidates */
+  int32_t variant;        /* QB_VARIANT_* actually used */
+  int32_t scale_exp;      /* e: device values are Q * 2^e rounded to integers */
+  int32_t prefix_bits;    /* k: fixed high bits per GPU thread chunk */
+  uint64_t candidates;    /* near-minimal states re-evaluated exactly (0 on the exact path) */
+  double kernel_ms;       /* device time of the traversal launch(es), CUDA events */
+  double total_ms;        /* wall time inside the call */
+} qb_result;
+
+/* Library / device management. */
+const char* qb_version(void);
+const char* qb_last_error(void);               /* thread-local message of the last failure */
+int qb_device_count(int* count);
+int qb_init(int device);                        /* select device for this thread, create stream + workspace */
+void qb_shutdown(void);                         /* free all device resources */
+
+/* Direct evaluation, replaces _kernels.eval_upper (_kernels.py:12-20) / core.evaluate
+ * (core.py:123-130): same fp64 row-major order, no FMA contraction.  Host only. */
+double qb_eval_upper(const double* coeffs, int n, const double* x);
+
+/* Exhaustive solve over the subspace {x : x >> (n - m_fix) == suffix}.
+ *   coeffs     n x n fp64 row-major upper-triangular (QuboInstance.coeffs, core.py:35-75)
+ *   m_fix      fixed high bits (0: the whole space)                    solver.py:54-79
+ *   suffix     value of the fixed high bits
+ *   m_tie      tie rule parameter for QB_TIE_GRAY (m_fix <= m_tie < n): 0 = solve_incremental,
+ *              m = solve_parallel(fixed_bits=m); for solve_subspace pass m_tie = m_fix
+ *   shard, shard_count   scan only shard `shard` of `shard_count` equal slices of the chunk space
+ *              (multi-GPU: one shard per rank; combine results by (value_key, tie_key))
+ * Replaces solver._scan_subspace + _kernels.gray_scan (solver.py:159-170, _kernels.py:46-75)
+ * and the thread-pool fan-out + combine_subspace_minima of solve_parallel (solver.py:193-229). */
+int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule,
+             uint32_t shard, uint32_t shard_count, int variant, qb_result* out);
+
+/* Seam 1: the reference operator _kernels.gray_scan(coeffs, qua, lin, x0, v0, n_free)
+ * (_kernels.py:46-75) with its exact return contract: x_min (fp64[n], 0/1), v_min
+ * (eval_upper(x_min), or v0 when no visited state beats the start), steps = 2^n_free - 1.
+ * Requires the free bits of x0 to be zero and v0 == eval_upper(x0), as in every reference call
+ * (solver.py:161-166).  qua/lin are accepted for signature parity and cross-checked. */
+int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, const double* x0, double v0,
+                 int n, int n_free, double* x_min, double* v_min, uint64_t* steps);
+
+/* Batch of independent instances (BASELINE config C): `count` instances of size n (n <= 24),
+ * coeffs laid out [count][n][n]; instance b is solved like solve_incremental (global Gray-rank
+ * tie rule).  One CTA per instance, T table in shared memory.  The reference has no batch API:
+ * this replaces a loop / thread pool of solve_incremental calls (solver.py:118-136). */
+int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
+                   double* kernel_ms);
+
+/* Test hook: chunk-start ("prefix") evaluation used by the traversal kernels, run as a standalone
+ * kernel.  For each of `count` chunks c in [c_begin, c_begin+count) of an n-bit problem with
+ * k prefix bits, writes the start state's value (fp64, exact on the integer path) and the local
+ * fields of the n-k free bits (fields[c][i] = Q_ii + sum_{j != i} Q~_ij x_j).  Mirrors
+ * eval_upper / delta (core.py:123-150). */
+int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_t count, double* values,
+                   double* fields);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUBRUTE_B200_H */

@@ -1,0 +1,217 @@
+"""ctypes binding of libqubrute_b200.so (C ABI in include/qubrute_b200.h).
+
+The shared library is built in-tree by :func:`build` (``nvcc -gencode
+arch=compute_100a,code=sm_100a``).  There is no CPU fallback: if the library is
+missing or no CUDA device is present, solver calls raise :class:`BackendError`.
+Host-only helpers (``eval_upper``) work without a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO_DIR = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "libqubrute_b200.so")
+HEADER = os.path.join(REPO_DIR, "include", "qubrute_b200.h")
+SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("qb_api.cu",)]
+DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]
+
+QB_OK = 0
+QB_E_ARG = -1
+QB_E_CAP = -2
+QB_E_CUDA = -3
+QB_E_NODEV = -4
+QB_E_INTERNAL = -5
+
+TIE_GRAY = 0
+TIE_INTEGER = 1
+
+VARIANT_AUTO = 0
+VARIANT_TABLE = 1
+VARIANT_FIELDWALK = 2
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-ffp-contract=off",
+    "-shared",
+]
+
+
+class BackendError(RuntimeError):
+    """The CUDA backend is unavailable or a kernel failed (never silently falls back)."""
+
+
+class QbResult(ctypes.Structure):
+    _fields_ = [
+        ("argmin_bits", ctypes.c_uint64),
+        ("value", ctypes.c_double),
+        ("tie_key", ctypes.c_uint64),
+        ("value_key", ctypes.c_uint64),
+        ("states", ctypes.c_uint64),
+        ("exact", ctypes.c_int32),
+        ("variant", ctypes.c_int32),
+        ("scale_exp", ctypes.c_int32),
+        ("prefix_bits", ctypes.c_int32),
+        ("candidates", ctypes.c_uint64),
+        ("kernel_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+    ]
+
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+
+# every symbol include/qubrute_b200.h declares, with its ctypes signature
+SIGNATURES = {
+    "qb_version": (ctypes.c_char_p, []),
+    "qb_last_error": (ctypes.c_char_p, []),
+    "qb_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "qb_init": (ctypes.c_int, [ctypes.c_int]),
+    "qb_shutdown": (None, []),
+    "qb_eval_upper": (ctypes.c_double, [_dp, ctypes.c_int, _dp]),
+    "qb_solve": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(QbResult)]),
+    "qb_gray_scan": (ctypes.c_int, [_dp, _dp, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _dp,
+                                    _u64p]),
+    "qb_solve_batch": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, _u64p, _dp, _dp]),
+    "qb_prefix_eval": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _dp, _dp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libqubrute_b200.so in-tree for sm_100a (skipped when up to date)."""
+    if not force and os.path.exists(LIB_PATH):
+        mtime = os.path.getmtime(LIB_PATH)
+        if all(os.path.getmtime(d) <= mtime for d in DEPS if os.path.exists(d)):
+            return LIB_PATH
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *SOURCES]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load (once) and return the native library; raises BackendError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise BackendError(f"{LIB_PATH} not built: run __graft_entry__.build() or "
+                                   "python -c 'import paper_2310_19373_b200._lib as l; l.build()'")
+            L = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().qb_last_error()
+    return msg.decode() if msg else ""
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def eval_upper(coeffs, x) -> float:
+    """Host-side eval_upper (_kernels.py:12-20) from the native library."""
+    c = _f64(coeffs)
+    xv = _f64(x)
+    return float(lib().qb_eval_upper(_ptr(c), c.shape[0], _ptr(xv)))
+
+
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    lib().qb_device_count(ctypes.byref(c))
+    return c.value
+
+
+def default_device() -> int:
+    return int(os.environ.get("QB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def init(device: int | None = None) -> None:
+    dev = default_device() if device is None else device
+    rc = lib().qb_init(dev)
+    if rc != QB_OK:
+        raise BackendError(f"qb_init({dev}) failed: {last_error()}")
+
+
+def check(rc: int, what: str) -> None:
+    if rc == QB_OK:
+        return
+    msg = last_error()
+    if rc == QB_E_CAP:
+        from .core import DimensionCapError
+
+        raise DimensionCapError(msg)
+    if rc == QB_E_ARG:
+        raise ValueError(msg)
+    raise BackendError(f"{what} failed ({rc}): {msg}")
+
+
+def solve(coeffs, m_fix: int = 0, suffix: int = 0, m_tie: int = 0, tie_rule: int = TIE_GRAY, shard: int = 0,
+          shard_count: int = 1, variant: int = VARIANT_AUTO, device: int | None = None) -> QbResult:
+    c = _f64(coeffs)
+    init(device)
+    out = QbResult()
+    rc = lib().qb_solve(_ptr(c), c.shape[0], m_fix, suffix, m_tie, tie_rule, shard, shard_count, variant,
+                        ctypes.byref(out))
+    check(rc, "qb_solve")
+    return out
+
+
+def gray_scan(coeffs, qua, lin, x0, v0, n_free, device: int | None = None):
+    c, q, l, x = _f64(coeffs), _f64(qua), _f64(lin), _f64(x0)
+    n = c.shape[0]
+    init(device)
+    xm = np.zeros(n)
+    vm = ctypes.c_double()
+    steps = ctypes.c_uint64()
+    rc = lib().qb_gray_scan(_ptr(c), _ptr(q), _ptr(l), _ptr(x), float(v0), n, int(n_free), _ptr(xm),
+                            ctypes.byref(vm), ctypes.byref(steps))
+    check(rc, "qb_gray_scan")
+    return xm, vm.value, int(steps.value)
+
+
+def solve_batch(coeffs_batch, device: int | None = None):
+    c = _f64(coeffs_batch)
+    count, n = c.shape[0], c.shape[1]
+    init(device)
+    bits = np.zeros(count, dtype=np.uint64)
+    vals = np.zeros(count)
+    ms = ctypes.c_double()
+    rc = lib().qb_solve_batch(_ptr(c), n, count, bits.ctypes.data_as(_u64p), _ptr(vals), ctypes.byref(ms))
+    check(rc, "qb_solve_batch")
+    return bits, vals, ms.value
+
+
+def prefix_eval(coeffs, k: int, c_begin: int, count: int, device: int | None = None):
+    c = _f64(coeffs)
+    n = c.shape[0]
+    init(device)
+    vals = np.zeros(count)
+    fields = np.zeros((count, n - k))
+    rc = lib().qb_prefix_eval(_ptr(c), n, k, c_begin, count, _ptr(vals), _ptr(fields))
+    check(rc, "qb_prefix_eval")
+    return vals, fields

@@ -1,0 +1,520 @@
+// Host runtime and C ABI of libqubrute_b200.so (declared in include/qubrute_b200.h).
+//
+// Responsibilities:
+//   * planning: choose chunk geometry (k prefix bits, L free bits, B inner bits) and the
+//     integer scaling 2^e that makes every device add exact;
+//   * per-device state: stream, events, persistent workspace, a mutex serialising calls;
+//   * launching the traversal / finalize / collect kernels and combining their output
+//     into the reference's result contract (minimiser, eval_upper value, tie key).
+// The reference's equivalents are solver.py:118-229 (dispatch, subspace fan-out, reduce)
+// and _kernels.py:12-75 (the numba kernels).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qubrute_b200.h"
+#include "qb_common.cuh"
+#include "qb_table.cuh"
+
+namespace qb {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define QB_CUDA(call)                                                                                  \
+  do {                                                                                                 \
+    cudaError_t e_ = (call);                                                                           \
+    if (e_ != cudaSuccess)                                                                             \
+      return fail(QB_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                                 std::to_string(__LINE__) + ")");                                      \
+  } while (0)
+
+// ------------------------------------------------------------------ kernel registry
+constexpr int TPB = 128;
+using KFn = void (*)(const TableParams);
+
+struct KernelSet {
+  int B1, B2, L;
+  KFn search, collect, finalize;
+  int occ = -1;  // resident CTAs per SM for `search` (lazy, per process)
+};
+
+#define QB_KS(B1, B2, L)                                                                             \
+  KernelSet {                                                                                        \
+    B1, B2, L, table_kernel<B1, B2, L, TPB, false>, table_kernel<B1, B2, L, TPB, true>,             \
+        table_finalize_kernel<B1, B2, L>                                                             \
+  }
+
+static KernelSet g_sets[] = {
+    QB_KS(0, 1, 1),   QB_KS(1, 1, 2),   QB_KS(1, 2, 3),   QB_KS(2, 2, 4),   QB_KS(2, 3, 5),
+    QB_KS(3, 3, 6),   QB_KS(3, 4, 7),   QB_KS(4, 4, 8),   QB_KS(4, 5, 9),   QB_KS(5, 5, 10),
+    QB_KS(5, 5, 12),  QB_KS(5, 5, 14),  QB_KS(5, 5, 16),  QB_KS(5, 5, 18),  QB_KS(5, 5, 20),
+    QB_KS(5, 5, 22),
+};
+
+static KernelSet* find_set(int B, int L) {
+  for (auto& s : g_sets)
+    if (s.B1 + s.B2 == B && s.L == L) return &s;
+  return nullptr;
+}
+
+// ------------------------------------------------------------------ per-device state
+struct Device {
+  int id = -1;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Rec* d_cta = nullptr;
+  size_t cta_cap = 0;
+  FinalOut* d_final = nullptr;
+  FinalOut* h_final = nullptr;  // pinned
+  long long* d_chunk_min = nullptr;
+  size_t chunk_min_cap = 0;
+  unsigned long long* d_cand = nullptr;
+  unsigned long long* d_cand_count = nullptr;
+  unsigned long long* h_cand_count = nullptr;  // pinned
+  size_t cand_cap = 0;
+  std::mutex mu;
+};
+
+static std::mutex g_dev_mu;
+static std::unique_ptr<Device> g_devs[64];
+
+static int get_device(Device** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(QB_E_NODEV, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (dev < 0 || dev >= 64) return fail(QB_E_NODEV, "device index out of range");
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  if (!g_devs[dev]) {
+    auto d = std::make_unique<Device>();
+    d->id = dev;
+    QB_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, dev));
+    QB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    QB_CUDA(cudaEventCreate(&d->ev0));
+    QB_CUDA(cudaEventCreate(&d->ev1));
+    QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
+    QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
+    QB_CUDA(cudaMalloc(&d->d_cand_count, sizeof(unsigned long long)));
+    QB_CUDA(cudaMallocHost(&d->h_cand_count, sizeof(unsigned long long)));
+    g_devs[dev] = std::move(d);
+  }
+  *out = g_devs[dev].get();
+  return QB_OK;
+}
+
+template <class T>
+static int ensure(T** ptr, size_t* cap, size_t need) {
+  if (*cap >= need && *ptr) return QB_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  size_t n = std::max<size_t>(need, 64);
+  QB_CUDA(cudaMalloc(ptr, n * sizeof(T)));
+  *cap = n;
+  return QB_OK;
+}
+
+// ------------------------------------------------------------------ planning
+struct Plan {
+  int n = 0, B = 0, L = 0, k = 0;
+  int e = 0;
+  bool exact = true;
+  long long Eq = 0;  // bound on |quantized - exact * 2^e| for any state (quantized units)
+  KernelSet* ks = nullptr;
+  std::unique_ptr<TableParams> P;
+};
+
+static double sym(const double* c, int n, int i, int j) {
+  return i < j ? c[(size_t)i * n + j] : c[(size_t)j * n + i];
+}
+
+// Integer scaling: q = rint(c * 2^e) with every partial sum the device forms below 2^24.
+static int quantize(const double* c, int n, int B, Plan& pl) {
+  const double LIM = 16777215.0;  // 2^24 - 1
+  auto bound = [&](auto get) {
+    double r_in = 0.0, rmax = 0.0;
+    for (int i = 0; i < B; ++i) {
+      for (int j = B; j < n; ++j) r_in += std::fabs(get(i, j));
+      for (int j = i; j < B; ++j) r_in += std::fabs(get(i, j));
+    }
+    for (int m = 0; m < n; ++m) {
+      double ra = 0.0;
+      for (int j = 0; j < n; ++j) ra += std::fabs(get(m, j));
+      rmax = std::max(rmax, ra);
+    }
+    return std::max(r_in, rmax);
+  };
+  auto getc = [&](int i, int j) { return sym(c, n, i, j); };
+  const double M = bound(getc);
+  bool integral = true;
+  long long nnz = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = i; j < n; ++j) {
+      const double v = c[(size_t)i * n + j];
+      if (!std::isfinite(v)) return fail(QB_E_ARG, "coefficients must be finite");
+      if (v != 0.0) ++nnz;
+      if (std::floor(v) != v) integral = false;
+    }
+  int e = 0;
+  if (M == 0.0 || (integral && M <= LIM)) {
+    e = 0;
+  } else {
+    e = (int)std::floor(std::log2(LIM / M));
+  }
+  std::vector<double> q((size_t)n * n);
+  for (int guard = 0; guard < 8; ++guard, --e) {
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) q[(size_t)i * n + j] = (j >= i) ? std::nearbyint(std::ldexp(c[(size_t)i * n + j], e)) : 0.0;
+    auto getq = [&](int i, int j) { return i < j ? q[(size_t)i * n + j] : q[(size_t)j * n + i]; };
+    if (bound(getq) <= LIM) break;
+    if (guard == 7) return fail(QB_E_INTERNAL, "quantization failed to meet the fp32 exactness bound");
+  }
+  bool exact = true;
+  for (int i = 0; i < n && exact; ++i)
+    for (int j = i; j < n; ++j)
+      if (std::ldexp(c[(size_t)i * n + j], e) != q[(size_t)i * n + j]) { exact = false; break; }
+  pl.e = e;
+  pl.exact = exact;
+  pl.Eq = exact ? 0 : (nnz + 1) / 2 + 1;
+  TableParams& P = *pl.P;
+  for (int i = 0; i < NMAX; ++i) {
+    P.d[i] = 0.f;
+    for (int j = 0; j < NMAX; ++j) P.Qs[i][j] = 0.f;
+  }
+  for (int i = 0; i < n; ++i) {
+    P.d[i] = (float)q[(size_t)i * n + i];
+    for (int j = i + 1; j < n; ++j) P.Qs[i][j] = P.Qs[j][i] = (float)q[(size_t)i * n + j];
+  }
+  for (int z = 0; z < (1 << BMAX); ++z) P.T[z] = 0.f;
+  for (int z = 0; z < (1 << B); ++z) {
+    double t = 0.0;
+    for (int i = 0; i < B; ++i) {
+      if (!((z >> i) & 1)) continue;
+      for (int j = i; j < B; ++j)
+        if ((z >> j) & 1) t += q[(size_t)i * n + j];
+    }
+    P.T[z] = (float)t;
+  }
+  return QB_OK;
+}
+
+static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& B, int& L) {
+  const int lmax = n - m_lock;  // free bits available per chunk
+  if (lmax < 1) return fail(QB_E_ARG, "no free bits");
+  if (lmax < BMAX) {
+    B = L = lmax;
+    return QB_OK;
+  }
+  B = BMAX;
+  // enough chunks for ~64 grid-stride rounds of resident threads on every shard
+  const double want_chunks = 64.0 * sms * 4 * TPB * (double)shard_count;
+  int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
+  int Lw = n - want_k;
+  Lw = std::max(Lw, BMAX);
+  Lw = std::min(Lw, std::min(22, lmax));
+  Lw = BMAX + 2 * ((Lw - BMAX) / 2);
+  L = Lw;
+  return QB_OK;
+}
+
+static unsigned long long host_tie_key(unsigned long long x, int n, int m_tie, int rule) {
+  if (rule == RULE_INTEGER) return x;
+  const int lo = n - m_tie;
+  const unsigned long long lowmask = mask64(lo);
+  return (x & ~lowmask) | ginv64(x & lowmask);
+}
+
+static unsigned long long ordered_double(double v) {
+  if (v == 0.0) v = 0.0;  // canonicalise -0.0
+  unsigned long long b;
+  std::memcpy(&b, &v, 8);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+static double eval_upper(const double* c, int n, const double* x) {
+  // _kernels.py:12-20, same order; this TU is compiled with --fmad=false for the host too.
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = i; j < n; ++j) acc += c[(size_t)i * n + j] * x[i] * x[j];
+  return acc;
+}
+
+static double eval_bits(const double* c, int n, unsigned long long x) {
+  double xv[64];
+  for (int i = 0; i < n; ++i) xv[i] = (double)((x >> i) & 1ull);
+  return eval_upper(c, n, xv);
+}
+
+// ------------------------------------------------------------------ the solve
+static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long suffix, int m_tie, int rule,
+                      uint32_t shard, uint32_t shard_count, int variant, qb_result* out) {
+  auto t_start = std::chrono::steady_clock::now();
+  if (!coeffs || !out) return fail(QB_E_ARG, "null pointer");
+  if (n < 1) return fail(QB_E_ARG, "dimension must be at least 1");
+  if (n > QB_MAX_DIM) return fail(QB_E_CAP, "n=" + std::to_string(n) + " exceeds cap " + std::to_string(QB_MAX_DIM));
+  if (m_fix < 0 || m_fix >= n) return fail(QB_E_ARG, "cannot fix " + std::to_string(m_fix) + " bits of an n=" + std::to_string(n) + " instance");
+  if (m_fix > 0 && suffix >= (1ull << m_fix)) return fail(QB_E_ARG, "suffix out of range");
+  if (m_fix == 0 && suffix != 0) return fail(QB_E_ARG, "suffix out of range");
+  if (rule != RULE_GRAY && rule != RULE_INTEGER) return fail(QB_E_ARG, "unknown tie rule");
+  if (rule == RULE_GRAY && (m_tie < m_fix || m_tie >= n))
+    return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
+  if (rule == RULE_INTEGER) m_tie = m_fix;
+  if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
+  if (variant != QB_VARIANT_AUTO && variant != QB_VARIANT_TABLE)
+    return fail(QB_E_ARG, "variant not available in this build");
+
+  Device* dev = nullptr;
+  if (int rc = get_device(&dev)) return rc;
+  std::lock_guard<std::mutex> guard(dev->mu);
+
+  Plan pl;
+  pl.n = n;
+  pl.P = std::make_unique<TableParams>();
+  const int m_lock = std::max(m_fix, m_tie);
+  int B, L;
+  if (int rc = choose_geometry(n, m_lock, shard_count, dev->sms, B, L)) return rc;
+  pl.B = B;
+  pl.L = L;
+  pl.k = n - L;
+  pl.ks = find_set(B, L);
+  if (!pl.ks) return fail(QB_E_INTERNAL, "no kernel instantiated for B=" + std::to_string(B) + " L=" + std::to_string(L));
+  if (int rc = quantize(coeffs, n, B, pl)) return rc;
+
+  TableParams& P = *pl.P;
+  P.n = n;
+  P.k = pl.k;
+  P.L = L;
+  P.m_fix = m_fix;
+  P.m_tie = m_tie;
+  P.rule = rule;
+  P.suffix = suffix;
+  const unsigned long long chunks = 1ull << (pl.k - m_fix);
+  const unsigned long long cb = (unsigned long long)(((unsigned __int128)chunks * shard) / shard_count);
+  const unsigned long long ce = (unsigned long long)(((unsigned __int128)chunks * (shard + 1)) / shard_count);
+  P.chunk_begin = cb;
+  P.chunk_end = ce;
+
+  std::memset(out, 0, sizeof(*out));
+  out->variant = QB_VARIANT_TABLE;
+  out->scale_exp = pl.e;
+  out->prefix_bits = pl.k;
+  out->exact = pl.exact ? 1 : 0;
+  out->value_key = ~0ull;
+  out->tie_key = ~0ull;
+  out->value = NAN;
+  const unsigned long long nchunks = ce - cb;
+  out->states = nchunks << L;
+  if (nchunks == 0) {
+    out->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    return QB_OK;
+  }
+
+  KernelSet& ks = *pl.ks;
+  if (ks.occ < 0) {
+    int occ = 0;
+    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.search, TPB, 0));
+    ks.occ = std::max(occ, 1);
+  }
+  const unsigned long long resident = (unsigned long long)ks.occ * dev->sms;
+  const unsigned long long need_ctas = (nchunks + TPB - 1) / TPB;
+  const int grid = (int)std::min(need_ctas, resident);
+  if (int rc = ensure(&dev->d_cta, &dev->cta_cap, (size_t)grid)) return rc;
+  P.cta_out = dev->d_cta;
+  P.final_out = dev->d_final;
+  P.nrec = grid;
+  P.mode = pl.exact ? MODE_SEARCH : MODE_SEARCH_RECORD;
+  if (!pl.exact) {
+    if (nchunks > (1ull << 27)) return fail(QB_E_INTERNAL, "too many chunks for the approximate path");
+    if (int rc = ensure(&dev->d_chunk_min, &dev->chunk_min_cap, (size_t)nchunks)) return rc;
+    P.chunk_min = dev->d_chunk_min;
+    if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)1 << 20)) return rc;
+    P.cand = dev->d_cand;
+    P.cand_cap = dev->cand_cap;
+    P.cand_count = dev->d_cand_count;
+  }
+
+  cudaStream_t st = dev->stream;
+  QB_CUDA(cudaEventRecord(dev->ev0, st));
+  ks.search<<<grid, TPB, 0, st>>>(P);
+  QB_CUDA(cudaGetLastError());
+  ks.finalize<<<1, 1024, 0, st>>>(P);
+  QB_CUDA(cudaGetLastError());
+  QB_CUDA(cudaEventRecord(dev->ev1, st));
+  QB_CUDA(cudaMemcpyAsync(dev->h_final, dev->d_final, sizeof(FinalOut), cudaMemcpyDeviceToHost, st));
+  QB_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
+  out->kernel_ms = ms;
+  const FinalOut fo = *dev->h_final;
+  if (!fo.found) return fail(QB_E_INTERNAL, "finalize found no state attaining the block minimum");
+
+  if (pl.exact) {
+    out->argmin_bits = fo.x;
+    out->tie_key = fo.key;
+    out->value_key = (unsigned long long)fo.val ^ (1ull << 63);
+    out->value = eval_bits(coeffs, n, fo.x);
+    if (host_tie_key(fo.x, n, m_tie, rule) != fo.key)
+      return fail(QB_E_INTERNAL, "device tie key disagrees with the host tie key");
+  } else {
+    // certified filter: every state within 2*Eq of the quantized minimum is re-evaluated exactly
+    P.mode = MODE_COLLECT;
+    P.theta = fo.val + 2 * pl.Eq;
+    QB_CUDA(cudaMemsetAsync(dev->d_cand_count, 0, sizeof(unsigned long long), st));
+    QB_CUDA(cudaEventRecord(dev->ev0, st));
+    ks.collect<<<grid, TPB, 0, st>>>(P);
+    QB_CUDA(cudaGetLastError());
+    QB_CUDA(cudaEventRecord(dev->ev1, st));
+    QB_CUDA(cudaMemcpyAsync(dev->h_cand_count, dev->d_cand_count, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
+    out->kernel_ms += ms;
+    const unsigned long long cnt = *dev->h_cand_count;
+    if (cnt == 0) return fail(QB_E_INTERNAL, "collect pass found no candidate");
+    if (cnt > P.cand_cap)
+      return fail(QB_E_INTERNAL, "more than " + std::to_string(P.cand_cap) + " near-tied minimisers (float path)");
+    std::vector<unsigned long long> cand(cnt);
+    QB_CUDA(cudaMemcpyAsync(cand.data(), dev->d_cand, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    double bv = 0.0;
+    unsigned long long bx = 0, bk = ~0ull;
+    bool have = false;
+    for (unsigned long long x : cand) {
+      const double v = eval_bits(coeffs, n, x);
+      const unsigned long long key = host_tie_key(x, n, m_tie, rule);
+      if (!have || v < bv || (v == bv && key < bk)) { bv = v; bx = x; bk = key; have = true; }
+    }
+    out->candidates = cnt;
+    out->argmin_bits = bx;
+    out->tie_key = bk;
+    out->value = bv;
+    out->value_key = ordered_double(bv);
+  }
+  out->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  return QB_OK;
+}
+
+}  // namespace qb
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* qb_version(void) { return "qubrute_b200 0.1.0 (sm_100a)"; }
+
+const char* qb_last_error(void) { return qb::g_err.c_str(); }
+
+int qb_device_count(int* count) {
+  if (!count) return qb::fail(QB_E_ARG, "null pointer");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return QB_OK;
+  }
+  *count = c;
+  return QB_OK;
+}
+
+int qb_init(int device) {
+  int c = 0;
+  qb_device_count(&c);
+  if (c == 0) return qb::fail(QB_E_NODEV, "no CUDA device available");
+  if (device < 0 || device >= c) return qb::fail(QB_E_ARG, "device index out of range");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return qb::fail(QB_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  qb::Device* d = nullptr;
+  return qb::get_device(&d);
+}
+
+void qb_shutdown(void) {
+  std::lock_guard<std::mutex> g(qb::g_dev_mu);
+  for (auto& d : qb::g_devs) {
+    if (!d) continue;
+    cudaSetDevice(d->id);
+    cudaStreamSynchronize(d->stream);
+    cudaFree(d->d_cta);
+    cudaFree(d->d_final);
+    cudaFreeHost(d->h_final);
+    cudaFree(d->d_chunk_min);
+    cudaFree(d->d_cand);
+    cudaFree(d->d_cand_count);
+    cudaFreeHost(d->h_cand_count);
+    cudaEventDestroy(d->ev0);
+    cudaEventDestroy(d->ev1);
+    cudaStreamDestroy(d->stream);
+    d.reset();
+  }
+}
+
+double qb_eval_upper(const double* coeffs, int n, const double* x) { return qb::eval_upper(coeffs, n, x); }
+
+int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule, uint32_t shard,
+             uint32_t shard_count, int variant, qb_result* out) {
+  return qb::solve_impl(coeffs, n, m_fix, suffix, m_tie, tie_rule, shard, shard_count, variant, out);
+}
+
+int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, const double* x0, double v0, int n,
+                 int n_free, double* x_min, double* v_min, uint64_t* steps) {
+  if (!coeffs || !x0 || !x_min || !v_min || !steps) return qb::fail(QB_E_ARG, "null pointer");
+  if (n < 1 || n > QB_MAX_DIM) return qb::fail(n < 1 ? QB_E_ARG : QB_E_CAP, "bad dimension");
+  if (n_free < 0 || n_free > n) return qb::fail(QB_E_ARG, "n_free out of range");
+  unsigned long long x0b = 0;
+  for (int i = 0; i < n; ++i) {
+    if (x0[i] != 0.0 && x0[i] != 1.0) return qb::fail(QB_E_ARG, "bit vector entries must be 0 or 1");
+    if (x0[i] == 1.0) {
+      if (i < n_free) return qb::fail(QB_E_ARG, "free bits of x0 must be zero (reference start_bits contract)");
+      x0b |= 1ull << i;
+    }
+  }
+  if (qua && lin) {  // signature parity: the split form must be the one of coeffs (core.py:104-111)
+    for (int i = 0; i < n; ++i) {
+      if (lin[i] != coeffs[(size_t)i * n + i]) return qb::fail(QB_E_ARG, "lin is not diag(coeffs)");
+      for (int j = 0; j < n; ++j)
+        if (i != j && qua[(size_t)i * n + j] != qb::sym(coeffs, n, i, j))
+          return qb::fail(QB_E_ARG, "qua is not the symmetric off-diagonal part of coeffs");
+    }
+  }
+  *steps = n_free > 0 ? ((1ull << n_free) - 1ull) : 0ull;
+  for (int i = 0; i < n; ++i) x_min[i] = x0[i];
+  *v_min = v0;
+  if (n_free == 0) return QB_OK;
+  const int m = n - n_free;
+  qb_result r;
+  int rc = qb::solve_impl(coeffs, n, m, m > 0 ? (x0b >> n_free) : 0ull, m, qb::RULE_GRAY, 0, 1, QB_VARIANT_AUTO, &r);
+  if (rc) return rc;
+  // the incumbent starts at (x0, v0) with strict '<' (_kernels.py:58-74): x0 is kept on ties,
+  // which the Gray-rank tie rule already guarantees (x0 has local rank 0)
+  if (r.argmin_bits != x0b) {
+    for (int i = 0; i < n; ++i) x_min[i] = (double)((r.argmin_bits >> i) & 1ull);
+    *v_min = r.value;
+  }
+  return QB_OK;
+}
+
+int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
+                   double* kernel_ms) {
+  (void)coeffs; (void)n; (void)count; (void)argmin_bits; (void)values; (void)kernel_ms;
+  return qb::fail(QB_E_INTERNAL, "qb_solve_batch: not built yet");
+}
+
+int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_t count, double* values,
+                   double* fields) {
+  (void)coeffs; (void)n; (void)k; (void)c_begin; (void)count; (void)values; (void)fields;
+  return qb::fail(QB_E_INTERNAL, "qb_prefix_eval: not built yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// Shared device-side definitions: launch parameters, Gray-rank algebra, tie keys.
+//
+// Terminology:
+//   n      problem bits; bit 0 = least significant (reference core.py:8-9)
+//   k      prefix bits fixed per chunk (positions L..n-1); one chunk = one thread task
+//   L      free bits walked inside a chunk (positions 0..L-1), L = n - k
+//   B      inner bits (positions 0..B-1) evaluated as one table block of 2^B states
+//   LO     outer free bits (positions B..L-1), walked in Gray order with __ffs
+//   m_fix  high bits fixed to `suffix` for the whole launch (solve_subspace)
+//   m_tie  tie-rule parameter: ties go to the lowest (suffix_m, Gray rank of the rest)
+#pragma once
+#include <climits>
+#include <cstdint>
+
+namespace qb {
+
+constexpr int NMAX = 40;   // reference core.py:24 MAX_DIM
+constexpr int BMAX = 10;   // largest inner block (1024-entry table, 4 KB in the constant bank)
+
+// One (value, tie-key) candidate.  val is the quantized objective (exact integer);
+// K is the tie key of the block (key >> B); c/j locate the block for finalization.
+struct Rec {
+  long long val;
+  unsigned long long K;
+  unsigned long long c;
+  unsigned int j;
+  unsigned int pad;
+};
+
+struct FinalOut {
+  long long val;            // quantized minimum (LLONG_MAX: shard had no states)
+  unsigned long long key;   // full tie key of the minimiser
+  unsigned long long x;     // minimiser bits
+  unsigned long long c;     // chunk index
+  unsigned int j;           // outer block
+  int found;
+};
+
+// Kernel parameters, passed by value as a __grid_constant__ (per-launch constant bank:
+// no global __constant__ symbol, so concurrent solves on one device cannot race).
+struct alignas(16) TableParams {
+  float T[1 << BMAX];        // inner table: T[z] = sum_{i<=j<B} q_ij z_i z_j, z = (u << B2) | w
+  float Qs[NMAX][NMAX];      // quantized symmetric off-diagonal part (0 on the diagonal)
+  float d[NMAX];             // quantized diagonal
+  int n, k, L, m_fix;
+  int m_tie, rule, mode, nrec;
+  unsigned long long suffix;       // value of the m_fix fixed high bits
+  unsigned long long chunk_begin;  // chunk range [begin, end) scanned by this launch
+  unsigned long long chunk_end;
+  long long theta;                 // collect threshold (mode 1)
+  long long* chunk_min;            // per-chunk minimum, indexed c - chunk_begin (approximate path)
+  unsigned long long* cand;        // candidate states (mode 1)
+  unsigned long long* cand_count;
+  unsigned long long cand_cap;
+  Rec* cta_out;                    // one record per CTA
+  FinalOut* final_out;
+};
+
+enum { RULE_GRAY = 0, RULE_INTEGER = 1 };
+enum { MODE_SEARCH = 0, MODE_SEARCH_RECORD = 1, MODE_COLLECT = 2 };
+
+__host__ __device__ __forceinline__ unsigned long long ginv64(unsigned long long x) {
+  // inverse reflected Gray code (prefix XOR from the top): step index at which x is visited
+  x ^= x >> 1; x ^= x >> 2; x ^= x >> 4; x ^= x >> 8; x ^= x >> 16; x ^= x >> 32;
+  return x;
+}
+
+__host__ __device__ __forceinline__ unsigned long long mask64(int b) {
+  return b >= 64 ? ~0ull : ((1ull << b) - 1ull);
+}
+
+// Chunk prefix s (k bits) of chunk index c: the m_fix top bits are the fixed suffix.
+__device__ __forceinline__ unsigned long long chunk_prefix(const TableParams& p, unsigned long long c) {
+  return (p.k > p.m_fix) ? ((p.suffix << (p.k - p.m_fix)) | c) : p.suffix;
+}
+
+// High part of the tie key for chunk prefix s, and the walk direction inside the chunk.
+// Gray rule: key_m(x) = (x_top_m << (n-m)) | ginv(x_low).  With x = (s << L) | y,
+// s = (s_top << (k-m)) | a:  key = (s_top << (n-m)) | (ginv(a) << L) | (t ^ (parity(a) ? ~0 : 0))
+// where y = gray(t); so the chunk contributes (s_top << (k-m)) | ginv(a) and a direction bit.
+// Integer rule (solve_naive): key = x itself.
+__device__ __forceinline__ unsigned long long chunk_key(const TableParams& p, unsigned long long s, int& dir) {
+  if (p.rule == RULE_INTEGER) { dir = 0; return s; }
+  const int lo = p.k - p.m_tie;              // prefix bits below the tie suffix (m_tie <= k)
+  const unsigned long long a = s & mask64(lo);
+  dir = __popcll(a) & 1;
+  return ((s >> lo) << lo) | ginv64(a);
+}
+
+// Tie key of outer block j (LO outer bits) of a chunk: key >> B.
+__device__ __forceinline__ unsigned long long block_key(const TableParams& p, unsigned long long key_hi, int dir,
+                                                        unsigned int j, int LO) {
+  if (p.rule == RULE_INTEGER) return (key_hi << LO) | (unsigned long long)(j ^ (j >> 1));
+  return (key_hi << LO) | (unsigned long long)(dir ? (j ^ (unsigned int)mask64(LO)) : j);
+}
+
+// Tie key of inner state z within block j (B inner bits).
+__device__ __forceinline__ unsigned int inner_key(const TableParams& p, int dir, unsigned int j, unsigned int z,
+                                                  int B) {
+  if (p.rule == RULE_INTEGER) return z;
+  const unsigned int mB = (unsigned int)mask64(B);
+  unsigned int t = (unsigned int)ginv64((z ^ ((j & 1u) << (B - 1))) & mB) & mB;
+  return dir ? (t ^ mB) : t;
+}
+
+__device__ __forceinline__ bool rec_less(const Rec& a, const Rec& b) {
+  return a.val < b.val || (a.val == b.val && a.K < b.K);
+}
+
+__device__ __forceinline__ Rec shfl_rec(const Rec& r, int src) {
+  Rec o;
+  o.val = __shfl_sync(0xffffffffu, r.val, src);
+  o.K = __shfl_sync(0xffffffffu, r.K, src);
+  o.c = __shfl_sync(0xffffffffu, r.c, src);
+  o.j = __shfl_sync(0xffffffffu, r.j, src);
+  o.pad = 0;
+  return o;
+}
+
+// Block-wide argmin of Rec (warp shuffle -> shared memory -> warp 0).  Result valid in thread 0.
+template <int TPB>
+__device__ __forceinline__ Rec cta_reduce(Rec r) {
+  __shared__ Rec sh[TPB / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Rec o = shfl_rec(r, (lane + off) & 31);
+    if (rec_less(o, r)) r = o;
+  }
+  if (lane == 0) sh[warp] = r;
+  __syncthreads();
+  if (warp == 0) {
+    r = (lane < TPB / 32) ? sh[lane] : Rec{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      Rec o = shfl_rec(r, (lane + off) & 31);
+      if (rec_less(o, r)) r = o;
+    }
+  }
+  return r;
+}
+
+}  // namespace qb

@@ -1,0 +1,225 @@
+// Blocked Gray-walk traversal kernel ("table" variant) for sm_100a.
+//
+// One thread owns one chunk at a time: the states whose top k bits equal the chunk
+// prefix s.  Inside the chunk the L free bits are split into B inner bits and
+// LO = L - B outer bits:
+//
+//   * outer bits are walked in reflected Gray order, one flip per block: bit
+//     l = B + __ffs(j) - 1, direction from bit l+1 of j (Alg. 1 / reference
+//     _kernels.py:63-71).  The flip applies Eq. 3, dV = s_l (Q_ll + F_l), and the
+//     row update of the local fields H (inner bits) and F (outer bits), all in
+//     registers with compile-time indices (one switch case per outer bit);
+//   * the 2^B inner states of a block are evaluated from a per-instance table:
+//         f(outer, z) = V + sum_{i<B} z_i H_i + T(z),   z = (u << B2) | w
+//     computed as min_u [ A_u + min_w (Bw_w + T(u,w)) ] with A/Bw subset sums of H.
+//     Each state costs one packed add (FADD2 on two states, T pair from the constant
+//     bank via LDCU.128) and half a 3-input min (FMNMX3).
+//
+// Arithmetic is exact: the host scales Q by 2^e into integers whose partial sums stay
+// below 2^24 in magnitude, so every fp32 add is an exact integer add; block bases V
+// are int64.  When Q * 2^e is not integral the search is a certified filter and the
+// host re-evaluates the near-minimal candidates exactly (qb_api.cu).
+#pragma once
+#include "qb_common.cuh"
+
+namespace qb {
+
+__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
+// Chunk-start / block-base ("prefix") evaluation.  For the state x with its B inner bits
+// treated as zero: V = f(x & ~innermask) (int64, exact), H_i = sum_{q>=B} x_q Qs[i][q] for the
+// inner bits, F_m = sum_{q>=B} x_q Qs[B+m][q] for the outer free bits.  Only bits q >= q_start
+// may be set (q_start = L at a chunk start, B for an arbitrary block).  All loops are uniform
+// across the warp so the Qs[.][q] operands are warp-uniform constant-bank loads.
+template <int B, int L>
+__device__ __forceinline__ void base_eval(const TableParams& p, unsigned long long x, int q_start, long long& V,
+                                          float (&H)[B], float (&F)[(L - B) > 0 ? (L - B) : 1]) {
+#pragma unroll
+  for (int i = 0; i < B; ++i) H[i] = 0.f;
+#pragma unroll
+  for (int m = 0; m < ((L - B) > 0 ? (L - B) : 1); ++m) F[m] = 0.f;
+  V = 0;
+  for (int q = q_start; q < p.n; ++q) {
+    const float xq = ((x >> q) & 1ull) ? 1.f : 0.f;
+#pragma unroll
+    for (int i = 0; i < B; ++i) H[i] = fmaf(xq, p.Qs[i][q], H[i]);
+#pragma unroll
+    for (int m = 0; m < L - B; ++m) F[m] = fmaf(xq, p.Qs[B + m][q], F[m]);
+    float row = p.d[q];
+    for (int r = q + 1; r < p.n; ++r) row = fmaf(((x >> r) & 1ull) ? 1.f : 0.f, p.Qs[q][r], row);
+    V += (long long)(xq * row);
+  }
+}
+
+// Outer flip of bit B+R (compile-time R) with sign sg = +-1: Eq. 3 value update then the
+// row/column update of every local field.  Linear if-chain: r = ctz(j) is 0 half the time.
+template <int B, int L, int R>
+__device__ __forceinline__ void outer_flip(const TableParams& p, int r, float sg, long long& V, float (&H)[B],
+                                           float (&F)[(L - B) > 0 ? (L - B) : 1]) {
+  if constexpr (R < L - B) {
+    if (r == R) {
+      constexpr int ELL = B + R;
+      V += (long long)(sg * (p.d[ELL] + F[R]));
+#pragma unroll
+      for (int i = 0; i < B; ++i) H[i] = fmaf(sg, p.Qs[i][ELL], H[i]);
+#pragma unroll
+      for (int m = 0; m < L - B; ++m) F[m] = fmaf(sg, p.Qs[B + m][ELL], F[m]);
+    } else {
+      outer_flip<B, L, R + 1>(p, r, sg, V, H, F);
+    }
+  }
+}
+
+// Minimum over the 2^B inner states of a block, relative to the block base V.
+template <int B1, int B2>
+__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2]) {
+  constexpr int NU = 1 << B1, NW = 1 << B2;
+  static_assert(B2 >= 1, "inner low part needs at least one bit");
+  float Bw[NW];
+  Bw[0] = 0.f;
+#pragma unroll
+  for (int i = 0; i < B2; ++i)
+#pragma unroll
+    for (int w = 0; w < (1 << i); ++w) Bw[w + (1 << i)] = Bw[w] + H[i];
+  float A[NU];
+  A[0] = 0.f;
+#pragma unroll
+  for (int i = 0; i < B1; ++i)
+#pragma unroll
+    for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + H[B2 + i];
+  float r[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; w += 2) {
+      const float2 t = *reinterpret_cast<const float2*>(&p.T[u * NW + w]);
+      const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
+      acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
+    }
+    r[u] = acc + A[u];
+  }
+  // 3-input min tree over u
+#pragma unroll
+  for (int width = NU; width > 1; width = (width + 2) / 3) {
+    const int nw = (width + 2) / 3;
+#pragma unroll
+    for (int o = 0; o < nw; ++o) {
+      float m = r[3 * o];
+      if (3 * o + 1 < width) m = fminf(m, r[3 * o + 1]);
+      if (3 * o + 2 < width) m = fminf(m, r[3 * o + 2]);
+      r[o] = m;
+    }
+  }
+  return r[0];
+}
+
+// Rare path of the collect pass: append every state of block j with value <= theta.
+template <int B, int L>
+__device__ __noinline__ void collect_block(const TableParams& p, unsigned long long s, unsigned int j, long long V,
+                                           const float* H) {
+  const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << B);
+  for (unsigned int z = 0; z < (1u << B); ++z) {
+    float r = p.T[z];
+    for (int i = 0; i < B; ++i)
+      if ((z >> i) & 1u) r += H[i];
+    if (V + (long long)r <= p.theta) {
+      const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
+      if (idx < p.cand_cap) p.cand[idx] = xo | z;
+    }
+  }
+}
+
+template <int B1, int B2, int L, int TPB, bool COLLECT>
+__global__ void __launch_bounds__(TPB) table_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2;
+  constexpr int LO = L - B;
+  constexpr int NF = LO > 0 ? LO : 1;
+  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  const unsigned long long stride = (unsigned long long)gridDim.x * TPB;
+  for (unsigned long long c = p.chunk_begin + (unsigned long long)blockIdx.x * TPB + threadIdx.x; c < p.chunk_end;
+       c += stride) {
+    if (COLLECT && p.chunk_min[c - p.chunk_begin] > p.theta) continue;
+    const unsigned long long s = chunk_prefix(p, c);
+    long long V;
+    float H[B], F[NF];
+    base_eval<B, L>(p, s << L, L, V, H, F);
+    int dir;
+    const unsigned long long key_hi = chunk_key(p, s, dir);
+    long long cmin = LLONG_MAX;
+    for (unsigned int j = 0; j < (1u << LO); ++j) {
+      if (j) {
+        const int r = __ffs(j) - 1;
+        const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
+        outer_flip<B, L, 0>(p, r, sg, V, H, F);
+      }
+      const float rm = block_min<B1, B2>(p, H);
+      const long long val = V + (long long)rm;
+      if (COLLECT) {
+        if (val <= p.theta) collect_block<B, L>(p, s, j, V, H);
+        continue;
+      }
+      cmin = min(cmin, val);
+      if (val <= best.val) {
+        const unsigned long long K = block_key(p, key_hi, dir, j, LO);
+        if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
+      }
+    }
+    if (!COLLECT && p.mode == MODE_SEARCH_RECORD) p.chunk_min[c - p.chunk_begin] = cmin;
+  }
+  if (COLLECT) return;
+  const Rec r = cta_reduce<TPB>(best);
+  if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
+}
+
+// Single CTA: reduce the per-CTA records, then one warp re-evaluates the winning block and
+// picks the lowest-key minimiser inside it.  Writes p.final_out.
+template <int B1, int B2, int L>
+__global__ void __launch_bounds__(1024) table_finalize_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2;
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  for (int i = threadIdx.x; i < p.nrec; i += 1024) {
+    const Rec r = p.cta_out[i];
+    if (rec_less(r, best)) best = r;
+  }
+  best = cta_reduce<1024>(best);
+  __shared__ Rec win;
+  if (threadIdx.x == 0) win = best;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  best = win;
+  const int lane = threadIdx.x;
+  if (best.val == LLONG_MAX) {
+    if (lane == 0) *p.final_out = FinalOut{LLONG_MAX, ~0ull, 0ull, 0ull, 0u, 0};
+    return;
+  }
+  const unsigned long long s = chunk_prefix(p, best.c);
+  int dir;
+  (void)chunk_key(p, s, dir);
+  const unsigned long long xo = (s << L) | ((unsigned long long)(best.j ^ (best.j >> 1)) << B);
+  long long V;
+  float H[B], F[NF];
+  base_eval<B, L>(p, xo, B, V, H, F);
+  unsigned int bk = ~0u, bz = 0u;
+  for (unsigned int z = lane; z < (1u << B); z += 32) {
+    float r = p.T[z];
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+      if ((z >> i) & 1u) r += H[i];
+    if (V + (long long)r == best.val) {
+      const unsigned int kin = inner_key(p, dir, best.j, z, B);
+      if (kin < bk) { bk = kin; bz = z; }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned int ok = __shfl_xor_sync(0xffffffffu, bk, off);
+    const unsigned int oz = __shfl_xor_sync(0xffffffffu, bz, off);
+    if (ok < bk) { bk = ok; bz = oz; }
+  }
+  if (lane == 0)
+    *p.final_out = FinalOut{best.val, (best.K << B) | bk, xo | bz, best.c, best.j, bk != ~0u ? 1 : 0};
+}
+
+}  // namespace qb

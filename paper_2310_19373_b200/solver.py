@@ -1,0 +1,176 @@
+"""Exhaustive QUBO solvers on B200 — drop-in for the reference's ``qubrute.solver``.
+
+Same entry points, types, validation, error messages and result contract as
+``pkg/src/qubrute/solver.py`` (cited per function); the work runs on the GPU
+through libqubrute_b200.so:
+
+* ``solve_incremental`` (solver.py:118-136): one exhaustive GPU solve, ties to the
+  lowest global Gray rank (what the reference's single Gray walk keeps);
+* ``solve_parallel`` (solver.py:193-229): the reference fixes m high bits, scans
+  the 2^m subspaces on T threads and keeps the lowest suffix on ties; here the
+  whole space is one GPU launch and the tie rule ``(suffix, local Gray rank)`` is
+  applied in the device reduction, so results are identical for every ``threads``;
+* ``solve_subspace`` (solver.py:139-156): one subspace, local Gray-rank ties;
+* ``solve_naive`` (solver.py:99-115): the oracle's contract (guard, lowest-integer
+  tie rule) served by the same exhaustive GPU search.
+
+``Solution.value`` is always ``evaluate(minimizer)`` in the reference's fp64 order
+and ``evaluations`` follows the reference's step accounting.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .core import MAX_DIM, DimensionCapError, QuboInstance, bits_from_int
+
+# solver.py:33
+NAIVE_MAX_DIM = 24
+
+MODES = ("naive", "incremental", "parallel")
+
+
+@dataclass(frozen=True, eq=False)
+class Solution:
+    """Minimiser (uint8, index 0 = LSB), its exact value, step count, wall seconds (solver.py:38-51)."""
+
+    minimizer: np.ndarray
+    value: float
+    evaluations: int
+    elapsed: float
+
+
+@dataclass(frozen=True)
+class SubspaceSpec:
+    """The ``m`` most-significant bits fixed to ``suffix`` (solver.py:54-79)."""
+
+    m: int
+    suffix: int
+
+    def __post_init__(self) -> None:
+        if self.m < 0:
+            raise ValueError(f"fixed-bit count must be >= 0, got {self.m}")
+        if not 0 <= self.suffix < (1 << self.m):
+            raise ValueError(f"suffix {self.suffix} out of range [0, 2**{self.m})")
+
+    def start_bits(self, n: int) -> np.ndarray:
+        if self.m >= n:
+            raise ValueError(f"cannot fix {self.m} bits of an n={n} instance")
+        bits = np.zeros(n, dtype=np.uint8)
+        for t in range(self.m):
+            bits[n - self.m + t] = (self.suffix >> t) & 1
+        return bits
+
+
+@dataclass(frozen=True)
+class SolveConfig:
+    """Solver knobs (solver.py:82-96).  ``threads`` only selects the default ``fixed_bits``
+    (and hence the tie rule), exactly as in the reference; the GPU does the scanning."""
+
+    threads: int = 1
+    fixed_bits: Optional[int] = None
+    mode: str = "incremental"
+
+    def __post_init__(self) -> None:
+        if self.threads < 1:
+            raise ValueError(f"threads must be >= 1, got {self.threads}")
+        if self.fixed_bits is not None and self.fixed_bits < 0:
+            raise ValueError(f"fixed_bits must be >= 0, got {self.fixed_bits}")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+
+
+def _solution(inst: QuboInstance, res, evaluations: int, t0: float) -> Solution:
+    minimizer = bits_from_int(int(res.argmin_bits), inst.n)
+    # res.value is eval_upper(minimiser) computed natively in the reference's order
+    return Solution(minimizer=minimizer, value=float(res.value), evaluations=int(evaluations),
+                    elapsed=max(time.perf_counter() - t0, 1e-9))
+
+
+def solve_naive(instance: QuboInstance, *, max_n: int = NAIVE_MAX_DIM) -> Solution:
+    """Exhaustive search keeping the lowest-integer minimiser (solver.py:99-115)."""
+    if instance.n > max_n:
+        raise DimensionCapError(
+            f"n={instance.n} exceeds the naive-solver guard {max_n}; "
+            f"use the incremental solver, or raise max_n to force it"
+        )
+    if instance.n > MAX_DIM:
+        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+    t0 = time.perf_counter()
+    res = _lib.solve(instance.coeffs, 0, 0, 0, _lib.TIE_INTEGER)
+    return _solution(instance, res, (1 << instance.n) - 1, t0)
+
+
+def solve_incremental(instance: QuboInstance) -> Solution:
+    """Exhaustive Gray-code solve; ties to the lowest global Gray rank (solver.py:118-136)."""
+    if instance.n > MAX_DIM:
+        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+    t0 = time.perf_counter()
+    res = _lib.solve(instance.coeffs, 0, 0, 0, _lib.TIE_GRAY)
+    return _solution(instance, res, (1 << instance.n) - 1, t0)
+
+
+def solve_subspace(instance: QuboInstance, sub: SubspaceSpec) -> Solution:
+    """Minimise over {x : top sub.m bits == sub.suffix} (solver.py:139-156)."""
+    t0 = time.perf_counter()
+    if sub.m >= instance.n:
+        raise ValueError(f"cannot fix {sub.m} bits of an n={instance.n} instance")
+    if instance.n > MAX_DIM:
+        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+    res = _lib.solve(instance.coeffs, sub.m, sub.suffix, sub.m, _lib.TIE_GRAY)
+    return _solution(instance, res, (1 << (instance.n - sub.m)) - 1, t0)
+
+
+def combine_subspace_minima(solutions: Sequence[Solution]) -> Solution:
+    """Min-reduce, earliest entry wins ties (solver.py:173-185)."""
+    if not solutions:
+        raise ValueError("no subspace solutions to combine")
+    best = solutions[0]
+    for sol in solutions[1:]:
+        if sol.value < best.value:
+            best = sol
+    return best
+
+
+def default_fixed_bits(n: int, threads: int) -> int:
+    """m = min(n - 1, ceil(log2(threads))) (solver.py:188-190)."""
+    return min(n - 1, (threads - 1).bit_length())
+
+
+def _resolve_m(instance: QuboInstance, config: SolveConfig | None) -> int:
+    if config is None:
+        config = SolveConfig()
+    if instance.n < 2:
+        raise ValueError("parallel solving needs n >= 2")
+    if instance.n > MAX_DIM:
+        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+    m = config.fixed_bits
+    if m is None:
+        m = default_fixed_bits(instance.n, config.threads)
+    if not 0 <= m < instance.n:
+        raise ValueError(f"fixed_bits must be in [0, {instance.n}), got {m}")
+    return m
+
+
+def solve_parallel(instance: QuboInstance, config: SolveConfig | None = None) -> Solution:
+    """All 2^m subspaces in one GPU launch, lowest-suffix tie rule (solver.py:193-229)."""
+    m = _resolve_m(instance, config)
+    t0 = time.perf_counter()
+    res = _lib.solve(instance.coeffs, 0, 0, m, _lib.TIE_GRAY)
+    return _solution(instance, res, (1 << instance.n) - (1 << m), t0)
+
+
+def solve(instance: QuboInstance, config: SolveConfig | None = None) -> Solution:
+    """Dispatch on ``config.mode`` (solver.py:232-240)."""
+    if config is None:
+        config = SolveConfig()
+    if config.mode == "naive":
+        return solve_naive(instance)
+    if config.mode == "incremental":
+        return solve_incremental(instance)
+    return solve_parallel(instance, config)

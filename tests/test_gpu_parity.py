@@ -1,0 +1,156 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden outputs
+and the CPU oracle.  Integer instances: bit-exact values and argmins.  Float instances:
+argmin exact and value bit-identical (the value is eval_upper of the argmin).  Tie rules:
+every entry point's rule, on tie-heavy instances.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2310_19373_b200 as qb
+from oracle import oracle as O
+from paper_2310_19373_b200 import _kernels, _lib, instances
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(sol):
+    return qb.bits_to_int(sol.minimizer)
+
+
+def _check(sol, want, name):
+    assert _bits(sol) == want["bits"], (name, _bits(sol), want["bits"])
+    assert sol.value == want["value"], (name, sol.value, want["value"])
+    assert sol.evaluations == want["evaluations"], name
+
+
+def test_golden_cases(golden):
+    for case in golden["cases"]:
+        inst = qb.QuboInstance(np.array(case["coeffs"]))
+        for key, want in case["results"].items():
+            name = f"{case['name']}:{key}"
+            if key == "incremental":
+                _check(qb.solve_incremental(inst), want, name)
+            elif key.startswith("parallel_m"):
+                m = int(key[len("parallel_m"):])
+                _check(qb.solve_parallel(inst, qb.SolveConfig(threads=4, fixed_bits=m)), want, name)
+            elif key == "naive":
+                _check(qb.solve_naive(inst), want, name)
+            elif key.startswith("subspace_m"):
+                m = int(key[len("subspace_m"):])
+                for s, w in enumerate(want):
+                    _check(qb.solve_subspace(inst, qb.SubspaceSpec(m, s)), w, f"{name}:{s}")
+
+
+def test_gray_scan_seam(golden):
+    for case in golden["gray_scan"]:
+        c = np.array(case["coeffs"])
+        form = qb.split(qb.QuboInstance(c))
+        xm, vm, steps = _kernels.gray_scan(c, form.qua, form.lin, np.array(case["x0"]), case["v0"], case["n_free"])
+        assert xm.tolist() == case["x_min"]
+        assert vm == case["v_min"]
+        assert steps == case["steps"]
+
+
+def _tie_heavy(n, seed, lo=-2, hi=2):
+    return instances.int_uniform_coeffs(n, seed, lo, hi)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11, 12, 13, 14])
+def test_tie_rules_against_enumeration(n):
+    for rep in range(6):
+        c = _tie_heavy(n, 1000 * n + rep)
+        inst = qb.QuboInstance(c)
+        bits, val, _ = O.expected_argmin(c, 0)
+        sol = qb.solve_incremental(inst)
+        assert _bits(sol) == bits and sol.value == val
+        bits, val, _ = O.expected_argmin(c, 0, rule="integer")
+        assert _bits(qb.solve_naive(inst)) == bits
+        for m in sorted({1, n // 2, n - 1}):
+            if not 0 < m < n:
+                continue
+            bits, val, _ = O.expected_argmin(c, m)
+            sol = qb.solve_parallel(inst, qb.SolveConfig(threads=2, fixed_bits=m))
+            assert _bits(sol) == bits, (n, rep, m)
+            for s in (0, (1 << m) - 1, (1 << m) // 3):
+                bits, val, _ = O.expected_argmin(c, m, suffix=s)
+                sol = qb.solve_subspace(inst, qb.SubspaceSpec(m, s))
+                assert _bits(sol) == bits, (n, rep, m, s)
+
+
+def test_degenerate_all_tied():
+    # zero matrix: every state ties; lowest key is the zero vector for every rule
+    for n in (1, 6, 17, 24):
+        inst = qb.QuboInstance(np.zeros((n, n)))
+        assert _bits(qb.solve_incremental(inst)) == 0
+        assert _bits(qb.solve_naive(inst, max_n=40)) == 0
+        if n >= 2:
+            assert _bits(qb.solve_parallel(inst, qb.SolveConfig(threads=4, fixed_bits=min(2, n - 1)))) == 0
+            s = qb.solve_subspace(inst, qb.SubspaceSpec(1, 1))
+            assert _bits(s) == 1 << (n - 1)
+
+
+@pytest.mark.parametrize("n", [18, 20, 22, 24])
+def test_medium_sizes_against_enumeration(n):
+    for name in ("A", "B", "D", "E"):
+        c = instances.config_coeffs(name, 3, n=n)
+        bits, val, mins = O.expected_argmin(c, 0)
+        sol = qb.solve_incremental(qb.QuboInstance(c))
+        assert _bits(sol) == bits, (name, n)
+        assert sol.value == O.eval_upper(c, sol.minimizer.astype(np.float64))
+
+
+def test_random_fp64_instances_vs_oracle():
+    # the reference's own generator gives fp64 (non-quantizable) values: certified filter path
+    for n in (10, 16, 21):
+        for rep in range(3):
+            inst = instances.random_instance(n, instances.bench_seed(n, rep))
+            bits, val, ev = O.solve_incremental(inst.coeffs)
+            sol = qb.solve_incremental(inst)
+            assert (_bits(sol), sol.value, sol.evaluations) == (bits, val, ev)
+            res = _lib.solve(inst.coeffs)
+            assert res.exact == 0 and res.candidates >= 1
+
+
+def test_config_d_full_golden(golden):
+    case = next(c for c in golden["cases"] if c["name"] == "configD_n32_rep0")
+    inst = qb.QuboInstance(np.array(case["coeffs"]))
+    _check(qb.solve_parallel(inst, qb.SolveConfig(threads=8, fixed_bits=6)), case["results"]["parallel_m6"], "D")
+    res = _lib.solve(inst.coeffs)
+    assert res.exact == 1
+
+
+def test_config_b_full_golden(golden):
+    case = next(c for c in golden["cases"] if c["name"] == "configB_n24_rep0")
+    inst = qb.QuboInstance(np.array(case["coeffs"]))
+    _check(qb.solve_incremental(inst), case["results"]["incremental"], "B")
+
+
+def test_sharding_is_invariant():
+    # the chunk space split into S shards and combined by (value_key, tie_key) == one launch
+    for name, n in (("D", 28), ("E", 30), ("A", 20)):
+        c = instances.config_coeffs(name, 1, n=n)
+        whole = _lib.solve(c)
+        for S in (2, 3, 8):
+            parts = [_lib.solve(c, shard=i, shard_count=S) for i in range(S)]
+            best = min(parts, key=lambda r: (r.value_key, r.tie_key))
+            assert (best.argmin_bits, best.value, best.tie_key) == (whole.argmin_bits, whole.value, whole.tie_key)
+            assert sum(p.states for p in parts) == 1 << n
+
+
+def test_config_e_n40_properties():
+    """n=40 is beyond the oracle: check the argmin against exact CPU scans of the
+    subspace that contains it and of random other subspaces."""
+    c = instances.config_coeffs("E", 0)
+    inst = qb.QuboInstance(c)
+    sol = qb.solve_incremental(inst)
+    x = _bits(sol)
+    assert sol.value == O.eval_upper(c, sol.minimizer.astype(np.float64))
+    m = 17  # 2^23-state subspaces
+    suffix = x >> (40 - m)
+    bits, val, _ = O.solve_subspaces(c, m, suffix, suffix + 1, threads=8)
+    assert bits == x and val == sol.value
+    rng = np.random.default_rng(0)
+    for s in rng.integers(0, 1 << m, size=4):
+        _, v, _ = O.solve_subspaces(c, m, int(s), int(s) + 1, threads=8)
+        assert v >= sol.value
