@@ -60,8 +60,13 @@ typedef struct qb_result {
   int32_t scale_exp;      /* e: device values are Q * 2^e rounded to integers */
   int32_t prefix_bits;    /* k: fixed high bits per GPU thread chunk */
   uint64_t candidates;    /* near-minimal states re-evaluated exactly (0 on the exact path) */
-  double kernel_ms;       /* device time of the traversal launch(es), CUDA events */
+  double kernel_ms;       /* device time of all launches of this call (CUDA events on the library stream) */
   double total_ms;        /* wall time inside the call */
+  double search_ms;       /* device time of the traversal (search) kernel alone */
+  double collect_ms;      /* device time of the candidate-collect kernel (0 on the exact path) */
+  int32_t launches;       /* kernels launched by this call */
+  int32_t reserved;
+  uint64_t param_bytes;   /* bytes of kernel parameters copied host->device per launch (Q, T tables) */
 } qb_result;
 
 /* Library / device management. */

@@ -62,6 +62,11 @@ class QbResult(ctypes.Structure):
         ("candidates", ctypes.c_uint64),
         ("kernel_ms", ctypes.c_double),
         ("total_ms", ctypes.c_double),
+        ("search_ms", ctypes.c_double),
+        ("collect_ms", ctypes.c_double),
+        ("launches", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("param_bytes", ctypes.c_uint64),
     ]
 
 

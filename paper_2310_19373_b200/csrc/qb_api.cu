@@ -75,7 +75,7 @@ struct Device {
   int id = -1;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
   Rec* d_cta = nullptr;
   size_t cta_cap = 0;
   FinalOut* d_final = nullptr;
@@ -105,6 +105,7 @@ static int get_device(Device** out) {
     QB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     QB_CUDA(cudaEventCreate(&d->ev0));
     QB_CUDA(cudaEventCreate(&d->ev1));
+    QB_CUDA(cudaEventCreate(&d->evs));
     QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
     QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
     QB_CUDA(cudaMalloc(&d->d_cand_count, sizeof(unsigned long long)));
@@ -350,6 +351,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   QB_CUDA(cudaEventRecord(dev->ev0, st));
   ks.search<<<grid, TPB, 0, st>>>(P);
   QB_CUDA(cudaGetLastError());
+  QB_CUDA(cudaEventRecord(dev->evs, st));
   ks.finalize<<<1, 1024, 0, st>>>(P);
   QB_CUDA(cudaGetLastError());
   QB_CUDA(cudaEventRecord(dev->ev1, st));
@@ -358,6 +360,10 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   float ms = 0.f;
   QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
   out->kernel_ms = ms;
+  QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->evs));
+  out->search_ms = ms;
+  out->launches = 2;
+  out->param_bytes = sizeof(TableParams);
   const FinalOut fo = *dev->h_final;
   if (!fo.found) return fail(QB_E_INTERNAL, "finalize found no state attaining the block minimum");
 
@@ -382,6 +388,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     QB_CUDA(cudaStreamSynchronize(st));
     QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
     out->kernel_ms += ms;
+    out->collect_ms = ms;
+    out->launches += 1;
     const unsigned long long cnt = *dev->h_cand_count;
     if (cnt == 0) return fail(QB_E_INTERNAL, "collect pass found no candidate");
     if (cnt > P.cand_cap)
@@ -455,6 +463,7 @@ void qb_shutdown(void) {
     cudaFreeHost(d->h_cand_count);
     cudaEventDestroy(d->ev0);
     cudaEventDestroy(d->ev1);
+    cudaEventDestroy(d->evs);
     cudaStreamDestroy(d->stream);
     d.reset();
   }

@@ -87,31 +87,26 @@ __device__ __forceinline__ float block_min(const TableParams& p, const float (&H
   for (int i = 0; i < B1; ++i)
 #pragma unroll
     for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + H[B2 + i];
-  float r[NU];
+  // running 3-input min over u (two u rows per FMNMX3); the per-u chains are independent
+  float rmin = 0.f;
 #pragma unroll
-  for (int u = 0; u < NU; ++u) {
-    float acc = 0.f;
+  for (int u = 0; u < NU; u += 2) {
+    float ru[2];
 #pragma unroll
-    for (int w = 0; w < NW; w += 2) {
-      const float2 t = *reinterpret_cast<const float2*>(&p.T[u * NW + w]);
-      const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
-      acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
+    for (int h = 0; h < 2; ++h) {
+      if (u + h >= NU) { ru[h] = ru[0]; continue; }
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; w += 2) {
+        const float2 t = *reinterpret_cast<const float2*>(&p.T[(u + h) * NW + w]);
+        const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
+        acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
+      }
+      ru[h] = acc + A[u + h];
     }
-    r[u] = acc + A[u];
+    rmin = (u == 0) ? fminf(ru[0], ru[1]) : fminf(fminf(rmin, ru[0]), ru[1]);
   }
-  // 3-input min tree over u
-#pragma unroll
-  for (int width = NU; width > 1; width = (width + 2) / 3) {
-    const int nw = (width + 2) / 3;
-#pragma unroll
-    for (int o = 0; o < nw; ++o) {
-      float m = r[3 * o];
-      if (3 * o + 1 < width) m = fminf(m, r[3 * o + 1]);
-      if (3 * o + 2 < width) m = fminf(m, r[3 * o + 2]);
-      r[o] = m;
-    }
-  }
-  return r[0];
+  return rmin;
 }
 
 // Rare path of the collect pass: append every state of block j with value <= theta.
