@@ -17,7 +17,7 @@ import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libqubrute_b200.so")
+LIB_PATH = os.environ.get("QB_LIB_PATH") or os.path.join(PKG_DIR, "libqubrute_b200.so")
 HEADER = os.path.join(REPO_DIR, "include", "qubrute_b200.h")
 SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("qb_api.cu",)]
 DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]

@@ -42,31 +42,44 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 // ------------------------------------------------------------------ kernel registry
-constexpr int TPB = 128;
+#ifndef QB_TPB
+#define QB_TPB 128
+#endif
+constexpr int TPB = QB_TPB;
 using KFn = void (*)(const TableParams);
 
 struct KernelSet {
-  int B1, B2, L;
+  int B1, B2, SB, L;
   KFn search, collect, finalize;
   int occ = -1;  // resident CTAs per SM for `search` (lazy, per process)
 };
 
-#define QB_KS(B1, B2, L)                                                                             \
-  KernelSet {                                                                                        \
-    B1, B2, L, table_kernel<B1, B2, L, TPB, false>, table_kernel<B1, B2, L, TPB, true>,             \
-        table_finalize_kernel<B1, B2, L>                                                             \
+#define QB_KS(B1, B2, SB, L)                                                                             \
+  KernelSet {                                                                                            \
+    B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB, false>, table_kernel<B1, B2, SB, L, TPB, true>,     \
+        table_finalize_kernel<B1, B2, SB, L>                                                             \
   }
 
+// Small problems (free bits < BIG_BE): one block of 2^L states per chunk, no sub-blocks.
+// Large problems: 2^10-entry table (BIG_BE = 10 block bits), L free bits per chunk.
+#ifndef QB_BIG_B1
+#define QB_BIG_B1 5
+#define QB_BIG_B2 5
+#endif
+constexpr int BIG_B1 = QB_BIG_B1, BIG_B2 = QB_BIG_B2, BIG_SB = 0, BIG_BE = BIG_B1 + BIG_B2 + BIG_SB;
 static KernelSet g_sets[] = {
-    QB_KS(0, 1, 1),   QB_KS(1, 1, 2),   QB_KS(1, 2, 3),   QB_KS(2, 2, 4),   QB_KS(2, 3, 5),
-    QB_KS(3, 3, 6),   QB_KS(3, 4, 7),   QB_KS(4, 4, 8),   QB_KS(4, 5, 9),   QB_KS(5, 5, 10),
-    QB_KS(5, 5, 12),  QB_KS(5, 5, 14),  QB_KS(5, 5, 16),  QB_KS(5, 5, 18),  QB_KS(5, 5, 20),
-    QB_KS(5, 5, 22),
+    QB_KS(0, 1, 0, 1),  QB_KS(1, 1, 0, 2),  QB_KS(1, 2, 0, 3),  QB_KS(2, 2, 0, 4),  QB_KS(2, 3, 0, 5),
+    QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KS(5, 5, 0, 10),
+#if QB_BIG_B1 + QB_BIG_B2 != 10
+    QB_KS(BIG_B1, BIG_B2, 0, BIG_BE),
+#endif
+    QB_KS(BIG_B1, BIG_B2, 0, 12), QB_KS(BIG_B1, BIG_B2, 0, 14), QB_KS(BIG_B1, BIG_B2, 0, 16),
+    QB_KS(BIG_B1, BIG_B2, 0, 18), QB_KS(BIG_B1, BIG_B2, 0, 20), QB_KS(BIG_B1, BIG_B2, 0, 22),
 };
 
-static KernelSet* find_set(int B, int L) {
+static KernelSet* find_set(int BE, int L) {
   for (auto& s : g_sets)
-    if (s.B1 + s.B2 == B && s.L == L) return &s;
+    if (s.B1 + s.B2 + s.SB == BE && s.L == L) return &s;
   return nullptr;
 }
 
@@ -130,7 +143,7 @@ static int ensure(T** ptr, size_t* cap, size_t need) {
 
 // ------------------------------------------------------------------ planning
 struct Plan {
-  int n = 0, B = 0, L = 0, k = 0;
+  int n = 0, B = 0, BE = 0, L = 0, k = 0;  // B: table bits, BE: block bits (table + sub-block)
   int e = 0;
   bool exact = true;
   long long Eq = 0;  // bound on |quantized - exact * 2^e| for any state (quantized units)
@@ -143,13 +156,14 @@ static double sym(const double* c, int n, int i, int j) {
 }
 
 // Integer scaling: q = rint(c * 2^e) with every partial sum the device forms below 2^24.
-static int quantize(const double* c, int n, int B, Plan& pl) {
+// BE: block bits (their relative values are formed in fp32); B: table bits (T is built over them).
+static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
   const double LIM = 16777215.0;  // 2^24 - 1
   auto bound = [&](auto get) {
     double r_in = 0.0, rmax = 0.0;
-    for (int i = 0; i < B; ++i) {
-      for (int j = B; j < n; ++j) r_in += std::fabs(get(i, j));
-      for (int j = i; j < B; ++j) r_in += std::fabs(get(i, j));
+    for (int i = 0; i < BE; ++i) {
+      for (int j = BE; j < n; ++j) r_in += std::fabs(get(i, j));
+      for (int j = i; j < BE; ++j) r_in += std::fabs(get(i, j));
     }
     for (int m = 0; m < n; ++m) {
       double ra = 0.0;
@@ -212,21 +226,21 @@ static int quantize(const double* c, int n, int B, Plan& pl) {
   return QB_OK;
 }
 
-static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& B, int& L) {
+static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& BE, int& L) {
   const int lmax = n - m_lock;  // free bits available per chunk
   if (lmax < 1) return fail(QB_E_ARG, "no free bits");
-  if (lmax < BMAX) {
-    B = L = lmax;
+  if (lmax <= BIG_BE) {
+    BE = L = std::min(lmax, BMAX);
     return QB_OK;
   }
-  B = BMAX;
+  BE = BIG_BE;
   // enough chunks for ~64 grid-stride rounds of resident threads on every shard
   const double want_chunks = 64.0 * sms * 4 * TPB * (double)shard_count;
   int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
   int Lw = n - want_k;
-  Lw = std::max(Lw, BMAX);
+  Lw = std::max(Lw, BIG_BE);
   Lw = std::min(Lw, std::min(22, lmax));
-  Lw = BMAX + 2 * ((Lw - BMAX) / 2);
+  if (Lw > 12) Lw = 2 * (Lw / 2);
   L = Lw;
   return QB_OK;
 }
@@ -285,14 +299,15 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   pl.n = n;
   pl.P = std::make_unique<TableParams>();
   const int m_lock = std::max(m_fix, m_tie);
-  int B, L;
-  if (int rc = choose_geometry(n, m_lock, shard_count, dev->sms, B, L)) return rc;
-  pl.B = B;
+  int BE, L;
+  if (int rc = choose_geometry(n, m_lock, shard_count, dev->sms, BE, L)) return rc;
+  pl.BE = BE;
   pl.L = L;
   pl.k = n - L;
-  pl.ks = find_set(B, L);
-  if (!pl.ks) return fail(QB_E_INTERNAL, "no kernel instantiated for B=" + std::to_string(B) + " L=" + std::to_string(L));
-  if (int rc = quantize(coeffs, n, B, pl)) return rc;
+  pl.ks = find_set(BE, L);
+  if (!pl.ks) return fail(QB_E_INTERNAL, "no kernel instantiated for BE=" + std::to_string(BE) + " L=" + std::to_string(L));
+  pl.B = pl.ks->B1 + pl.ks->B2;
+  if (int rc = quantize(coeffs, n, BE, pl.B, pl)) return rc;
 
   TableParams& P = *pl.P;
   P.n = n;

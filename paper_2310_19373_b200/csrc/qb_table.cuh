@@ -22,6 +22,10 @@
 #pragma once
 #include "qb_common.cuh"
 
+#ifndef QB_MINB
+#define QB_MINB 5  // resident CTAs per SM requested from ptxas: caps registers at 96 (20 warps/SM)
+#endif
+
 namespace qb {
 
 __device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) { return __fadd2_rn(a, b); }
@@ -51,85 +55,135 @@ __device__ __forceinline__ void base_eval(const TableParams& p, unsigned long lo
   }
 }
 
-// Outer flip of bit B+R (compile-time R) with sign sg = +-1: Eq. 3 value update then the
-// row/column update of every local field.  Linear if-chain: r = ctz(j) is 0 half the time.
-template <int B, int L, int R>
-__device__ __forceinline__ void outer_flip(const TableParams& p, int r, float sg, long long& V, float (&H)[B],
+// Outer flip of bit ELL (compile-time in each branch; runtime `ell` selects it) with sign
+// sg = +-1: Eq. 3 value update, then the row/column update of every local field (H: table bits,
+// F: bits [B, L)).  Linear if-chain from the lowest outer bit: ctz(j) is 0 half the time.
+template <int B, int L, int ELL>
+__device__ __forceinline__ void outer_flip(const TableParams& p, int ell, float sg, long long& V, float (&H)[B],
                                            float (&F)[(L - B) > 0 ? (L - B) : 1]) {
-  if constexpr (R < L - B) {
-    if (r == R) {
-      constexpr int ELL = B + R;
-      V += (long long)(sg * (p.d[ELL] + F[R]));
+  if constexpr (ELL < L) {
+    if (ell == ELL) {
+      V += (long long)(sg * (p.d[ELL] + F[ELL - B]));
 #pragma unroll
       for (int i = 0; i < B; ++i) H[i] = fmaf(sg, p.Qs[i][ELL], H[i]);
 #pragma unroll
       for (int m = 0; m < L - B; ++m) F[m] = fmaf(sg, p.Qs[B + m][ELL], F[m]);
     } else {
-      outer_flip<B, L, R + 1>(p, r, sg, V, H, F);
+      outer_flip<B, L, ELL + 1>(p, ell, sg, V, H, F);
     }
   }
 }
 
-// Minimum over the 2^B inner states of a block, relative to the block base V.
-template <int B1, int B2>
-__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2]) {
-  constexpr int NU = 1 << B1, NW = 1 << B2;
+__host__ __device__ constexpr int ctz_c(int k) { return (k & 1) ? 0 : 1 + ctz_c(k >> 1); }
+
+// Minimum over the 2^(B+SB) states of a super-block, relative to its base value V (all block
+// bits zero).  The B table bits are split into u (B1 high) and w (B2 low); the SB sub-block
+// bits (positions B..B+SB-1) select one of P = 2^SB sub-blocks that share every table load:
+//     f(s, u, w) = V + delta_s + A^s_u + Bw^s_w + T(u, w)
+// with H^s = H + Q[.][sub bits of s], Bw^s = subset sums of H^s over w, A^s walked over u in
+// Gray order, delta_s = the sub-block bits' own value given the outer state (uses F).
+// Per state: half an FADD2 (two states, T pair from the constant bank through uniform
+// registers), half an FMNMX3, and 1/(2P) of an LDCU.128.
+template <int B1, int B2, int SB, int NF>
+__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
+  constexpr int B = B1 + B2, NU = 1 << B1, NW = 1 << B2, P = 1 << SB;
   static_assert(B2 >= 1, "inner low part needs at least one bit");
-  float Bw[NW];
-  Bw[0] = 0.f;
-#pragma unroll
-  for (int i = 0; i < B2; ++i)
-#pragma unroll
-    for (int w = 0; w < (1 << i); ++w) Bw[w + (1 << i)] = Bw[w] + H[i];
-  float A[NU];
-  A[0] = 0.f;
-#pragma unroll
-  for (int i = 0; i < B1; ++i)
-#pragma unroll
-    for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + H[B2 + i];
-  // running 3-input min over u (two u rows per FMNMX3); the per-u chains are independent
   float rmin = 0.f;
 #pragma unroll
-  for (int u = 0; u < NU; u += 2) {
-    float ru[2];
+  for (int s = 0; s < P; ++s) {
+    float hs[B];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (u + h >= NU) { ru[h] = ru[0]; continue; }
-      float acc = 0.f;
+    for (int i = 0; i < B; ++i) {
+      float h = H[i];
 #pragma unroll
-      for (int w = 0; w < NW; w += 2) {
-        const float2 t = *reinterpret_cast<const float2*>(&p.T[(u + h) * NW + w]);
-        const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
-        acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
-      }
-      ru[h] = acc + A[u + h];
+      for (int t = 0; t < SB; ++t)
+        if ((s >> t) & 1) h += p.Qs[i][B + t];
+      hs[i] = h;
     }
-    rmin = (u == 0) ? fminf(ru[0], ru[1]) : fminf(fminf(rmin, ru[0]), ru[1]);
+    float dl = 0.f;
+#pragma unroll
+    for (int t = 0; t < SB; ++t) {
+      if (!((s >> t) & 1)) continue;
+      dl += p.d[B + t] + F[t];
+#pragma unroll
+      for (int t2 = t + 1; t2 < SB; ++t2)
+        if ((s >> t2) & 1) dl += p.Qs[B + t][B + t2];
+    }
+    // subset sums: Bw over the w bits, A over the u bits (independent adds, no serial chain)
+    float Bw[NW];
+    Bw[0] = 0.f;
+#pragma unroll
+    for (int i = 0; i < B2; ++i)
+#pragma unroll
+      for (int w = 0; w < (1 << i); ++w) Bw[w + (1 << i)] = Bw[w] + hs[i];
+    float A[NU];
+    A[0] = dl;
+#pragma unroll
+    for (int i = 0; i < B1; ++i)
+#pragma unroll
+      for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + hs[B2 + i];
+#pragma unroll
+    for (int u = 0; u < NU; u += 2) {
+      float ru[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (u + h >= NU) { ru[h] = ru[0]; continue; }
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; w += 2) {
+          const float2 t = *reinterpret_cast<const float2*>(&p.T[(u + h) * NW + w]);
+          const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
+          acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
+        }
+        ru[h] = acc + A[u + h];
+      }
+      rmin = (s == 0 && u == 0) ? fminf(ru[0], ru[1]) : fminf(fminf(rmin, ru[0]), ru[1]);
+    }
   }
   return rmin;
 }
 
-// Rare path of the collect pass: append every state of block j with value <= theta.
-template <int B, int L>
-__device__ __noinline__ void collect_block(const TableParams& p, unsigned long long s, unsigned int j, long long V,
-                                           const float* H) {
-  const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << B);
-  for (unsigned int z = 0; z < (1u << B); ++z) {
-    float r = p.T[z];
-    for (int i = 0; i < B; ++i)
-      if ((z >> i) & 1u) r += H[i];
-    if (V + (long long)r <= p.theta) {
-      const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
-      if (idx < p.cand_cap) p.cand[idx] = xo | z;
+// Every state of super-block j of chunk prefix s, evaluated directly from its base (finalize and
+// collect; rare).  Calls fn(z_block, value) for the 2^(B+SB) states, z_block = (sub << B) | z.
+template <int B, int SB, int L, class Fn>
+__device__ __forceinline__ void for_block_states(const TableParams& p, unsigned long long xo, int lane, int lanes,
+                                                 Fn&& fn) {
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+#pragma unroll 1
+  for (int sb = 0; sb < (1 << SB); ++sb) {
+    long long V;
+    float H[B], F[NF];
+    base_eval<B, L>(p, xo | ((unsigned long long)sb << B), B, V, H, F);
+#pragma unroll 1
+    for (unsigned int z = lane; z < (1u << B); z += lanes) {
+      float r = p.T[z];
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+        if ((z >> i) & 1u) r += H[i];
+      fn(((unsigned int)sb << B) | z, V + (long long)r);
     }
   }
 }
 
-template <int B1, int B2, int L, int TPB, bool COLLECT>
-__global__ void __launch_bounds__(TPB) table_kernel(const __grid_constant__ TableParams p) {
+template <int B, int SB, int L>
+__device__ __noinline__ void collect_block(const TableParams& p, unsigned long long s, unsigned int j) {
+  constexpr int BE = B + SB;
+  const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
+  for_block_states<B, SB, L>(p, xo, 0, 1, [&](unsigned int zb, long long val) {
+    if (val <= p.theta) {
+      const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
+      if (idx < p.cand_cap) p.cand[idx] = xo | zb;
+    }
+  });
+}
+
+template <int B1, int B2, int SB, int L, int TPB, bool COLLECT>
+__global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
-  constexpr int LO = L - B;
-  constexpr int NF = LO > 0 ? LO : 1;
+  constexpr int BE = B + SB;
+  constexpr int LO = L - BE;
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  static_assert(LO >= 0, "block bits exceed chunk bits");
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   const unsigned long long stride = (unsigned long long)gridDim.x * TPB;
   for (unsigned long long c = p.chunk_begin + (unsigned long long)blockIdx.x * TPB + threadIdx.x; c < p.chunk_end;
@@ -146,12 +200,12 @@ __global__ void __launch_bounds__(TPB) table_kernel(const __grid_constant__ Tabl
       if (j) {
         const int r = __ffs(j) - 1;
         const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
-        outer_flip<B, L, 0>(p, r, sg, V, H, F);
+        outer_flip<B, L, BE>(p, BE + r, sg, V, H, F);
       }
-      const float rm = block_min<B1, B2>(p, H);
+      const float rm = block_min<B1, B2, SB, NF>(p, H, F);
       const long long val = V + (long long)rm;
       if (COLLECT) {
-        if (val <= p.theta) collect_block<B, L>(p, s, j, V, H);
+        if (val <= p.theta) collect_block<B, SB, L>(p, s, j);
         continue;
       }
       cmin = min(cmin, val);
@@ -167,12 +221,12 @@ __global__ void __launch_bounds__(TPB) table_kernel(const __grid_constant__ Tabl
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
 }
 
-// Single CTA: reduce the per-CTA records, then one warp re-evaluates the winning block and
+// Single CTA: reduce the per-CTA records, then one warp re-evaluates the winning super-block and
 // picks the lowest-key minimiser inside it.  Writes p.final_out.
-template <int B1, int B2, int L>
+template <int B1, int B2, int SB, int L>
 __global__ void __launch_bounds__(1024) table_finalize_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
-  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  constexpr int BE = B + SB;
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   for (int i = threadIdx.x; i < p.nrec; i += 1024) {
     const Rec r = p.cta_out[i];
@@ -192,21 +246,16 @@ __global__ void __launch_bounds__(1024) table_finalize_kernel(const __grid_const
   const unsigned long long s = chunk_prefix(p, best.c);
   int dir;
   (void)chunk_key(p, s, dir);
-  const unsigned long long xo = (s << L) | ((unsigned long long)(best.j ^ (best.j >> 1)) << B);
-  long long V;
-  float H[B], F[NF];
-  base_eval<B, L>(p, xo, B, V, H, F);
+  const unsigned long long xo = (s << L) | ((unsigned long long)(best.j ^ (best.j >> 1)) << BE);
   unsigned int bk = ~0u, bz = 0u;
-  for (unsigned int z = lane; z < (1u << B); z += 32) {
-    float r = p.T[z];
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-      if ((z >> i) & 1u) r += H[i];
-    if (V + (long long)r == best.val) {
-      const unsigned int kin = inner_key(p, dir, best.j, z, B);
-      if (kin < bk) { bk = kin; bz = z; }
+  const unsigned int jj = best.j;
+  const long long target = best.val;
+  for_block_states<B, SB, L>(p, xo, lane, 32, [&](unsigned int zb, long long val) {
+    if (val == target) {
+      const unsigned int kin = inner_key(p, dir, jj, zb, BE);
+      if (kin < bk) { bk = kin; bz = zb; }
     }
-  }
+  });
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned int ok = __shfl_xor_sync(0xffffffffu, bk, off);
@@ -214,7 +263,7 @@ __global__ void __launch_bounds__(1024) table_finalize_kernel(const __grid_const
     if (ok < bk) { bk = ok; bz = oz; }
   }
   if (lane == 0)
-    *p.final_out = FinalOut{best.val, (best.K << B) | bk, xo | bz, best.c, best.j, bk != ~0u ? 1 : 0};
+    *p.final_out = FinalOut{best.val, (best.K << BE) | bk, xo | bz, best.c, best.j, bk != ~0u ? 1 : 0};
 }
 
 }  // namespace qb
