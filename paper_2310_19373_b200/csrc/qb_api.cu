@@ -23,6 +23,7 @@
 #include "../../include/qubrute_b200.h"
 #include "qb_common.cuh"
 #include "qb_table.cuh"
+#include "qb_batch.cuh"
 
 namespace qb {
 
@@ -47,17 +48,19 @@ static int fail(int code, const std::string& msg) {
 #endif
 constexpr int TPB = QB_TPB;
 using KFn = void (*)(const TableParams);
+using PFn = void (*)(const TableParams, double*, double*, int);
 
 struct KernelSet {
   int B1, B2, SB, L;
   KFn search, collect, finalize;
+  PFn prefix;
   int occ = -1;  // resident CTAs per SM for `search` (lazy, per process)
 };
 
 #define QB_KS(B1, B2, SB, L)                                                                             \
   KernelSet {                                                                                            \
     B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB, false>, table_kernel<B1, B2, SB, L, TPB, true>,     \
-        table_finalize_kernel<B1, B2, SB, L>                                                             \
+        table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>                          \
   }
 
 // Small problems (free bits < BIG_BE): one block of 2^L states per chunk, no sub-blocks.
@@ -99,6 +102,10 @@ struct Device {
   unsigned long long* d_cand_count = nullptr;
   unsigned long long* h_cand_count = nullptr;  // pinned
   size_t cand_cap = 0;
+  double* d_batch_coeffs = nullptr;
+  size_t batch_coeffs_cap = 0;
+  BatchOut* d_batch_out = nullptr;
+  size_t batch_out_cap = 0;
   std::mutex mu;
 };
 
@@ -430,6 +437,107 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   return QB_OK;
 }
 
+// ------------------------------------------------------------------ prefix-evaluation hook
+static int prefix_impl(const double* coeffs, int n, int k, uint64_t c_begin, uint64_t count, double* values,
+                       double* fields) {
+  if (!coeffs || !values || !fields) return fail(QB_E_ARG, "null pointer");
+  if (n < 1 || n > QB_MAX_DIM) return fail(n < 1 ? QB_E_ARG : QB_E_CAP, "bad dimension");
+  if (k < 0 || k >= n) return fail(QB_E_ARG, "k out of range");
+  const int L = n - k;
+  KernelSet* ks = nullptr;
+  for (auto& s : g_sets)
+    if (s.L == L && (L <= BIG_BE ? s.B1 + s.B2 + s.SB == L : s.B1 == BIG_B1 && s.B2 == BIG_B2)) ks = &s;
+  if (!ks) return fail(QB_E_ARG, "no traversal kernel with L = n - k = " + std::to_string(L));
+  if (c_begin + count > (1ull << k) || count == 0) return fail(QB_E_ARG, "chunk range out of range");
+  Device* dev = nullptr;
+  if (int rc = get_device(&dev)) return rc;
+  std::lock_guard<std::mutex> guard(dev->mu);
+  Plan pl;
+  pl.P = std::make_unique<TableParams>();
+  const int B = ks->B1 + ks->B2;
+  if (int rc = quantize(coeffs, n, B + ks->SB, B, pl)) return rc;
+  TableParams& P = *pl.P;
+  P.n = n; P.k = k; P.L = L; P.m_fix = 0; P.m_tie = 0; P.rule = RULE_GRAY; P.suffix = 0;
+  P.chunk_begin = c_begin;
+  P.chunk_end = c_begin + count;
+  double *dv = nullptr, *df = nullptr;
+  QB_CUDA(cudaMalloc(&dv, count * sizeof(double)));
+  QB_CUDA(cudaMalloc(&df, count * L * sizeof(double)));
+  cudaStream_t st = dev->stream;
+  ks->prefix<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(P, dv, df, pl.e);
+  cudaError_t e1 = cudaGetLastError();
+  cudaError_t e2 = cudaMemcpyAsync(values, dv, count * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaError_t e3 = cudaMemcpyAsync(fields, df, count * L * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaError_t e4 = cudaStreamSynchronize(st);
+  cudaFree(dv);
+  cudaFree(df);
+  for (cudaError_t e : {e1, e2, e3, e4})
+    if (e != cudaSuccess) return fail(QB_E_CUDA, std::string("qb_prefix_eval: ") + cudaGetErrorString(e));
+  return QB_OK;
+}
+
+// ------------------------------------------------------------------ batch (config C)
+using BatchFn = void (*)(const BatchParams);
+static const BatchFn g_batch[] = {nullptr,
+                                  batch_kernel<0, 1>, batch_kernel<1, 1>, batch_kernel<1, 2>, batch_kernel<2, 2>,
+                                  batch_kernel<2, 3>, batch_kernel<3, 3>, batch_kernel<3, 4>, batch_kernel<4, 4>,
+                                  batch_kernel<4, 5>, batch_kernel<5, 5>};
+
+static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
+                      double* kernel_ms) {
+  if (!coeffs || !argmin_bits || !values) return fail(QB_E_ARG, "null pointer");
+  if (n < 1) return fail(QB_E_ARG, "dimension must be at least 1");
+  if (n > BATCH_NMAX) return fail(QB_E_CAP, "batch path supports n <= " + std::to_string(BATCH_NMAX));
+  if (count == 0) return QB_OK;
+  if (count > (1ull << 31) - 1) return fail(QB_E_ARG, "count too large");
+  for (uint64_t i = 0; i < count * (uint64_t)n * n; ++i)
+    if (!std::isfinite(coeffs[i])) return fail(QB_E_ARG, "coefficients must be finite");
+  Device* dev = nullptr;
+  if (int rc = get_device(&dev)) return rc;
+  std::vector<uint64_t> fallback;
+  {
+    std::lock_guard<std::mutex> guard(dev->mu);
+    const size_t nc = (size_t)count * n * n;
+    if (int rc = ensure(&dev->d_batch_coeffs, &dev->batch_coeffs_cap, nc)) return rc;
+    if (int rc = ensure(&dev->d_batch_out, &dev->batch_out_cap, (size_t)count)) return rc;
+    cudaStream_t st = dev->stream;
+    QB_CUDA(cudaMemcpyAsync(dev->d_batch_coeffs, coeffs, nc * sizeof(double), cudaMemcpyHostToDevice, st));
+    const int B = std::min(n, BMAX);
+    const unsigned chunks = 1u << (n - B);
+    int threads = (int)std::min<unsigned>(BATCH_TPB_MAX, std::max<unsigned>(32u, chunks));
+    threads = (threads + 31) / 32 * 32;
+    BatchParams bp{dev->d_batch_coeffs, dev->d_batch_out, n, (int)count};
+    QB_CUDA(cudaEventRecord(dev->ev0, st));
+    g_batch[B]<<<(unsigned)count, threads, 0, st>>>(bp);
+    QB_CUDA(cudaGetLastError());
+    QB_CUDA(cudaEventRecord(dev->ev1, st));
+    std::vector<BatchOut> out(count);
+    QB_CUDA(cudaMemcpyAsync(out.data(), dev->d_batch_out, count * sizeof(BatchOut), cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
+    if (kernel_ms) *kernel_ms = ms;
+    for (uint64_t b = 0; b < count; ++b) {
+      if (out[b].status == 0) {
+        argmin_bits[b] = out[b].x;
+        values[b] = out[b].value;
+      } else if (out[b].status == 1) {
+        fallback.push_back(b);
+      } else {
+        return fail(QB_E_INTERNAL, "batch kernel found no candidate for instance " + std::to_string(b));
+      }
+    }
+  }
+  // instances with more than BATCH_CAP near-tied minimisers: full single-instance path
+  for (uint64_t b : fallback) {
+    qb_result r;
+    if (int rc = solve_impl(coeffs + b * (uint64_t)n * n, n, 0, 0, 0, RULE_GRAY, 0, 1, QB_VARIANT_AUTO, &r)) return rc;
+    argmin_bits[b] = r.argmin_bits;
+    values[b] = r.value;
+  }
+  return QB_OK;
+}
+
 }  // namespace qb
 
 // ====================================================================== C ABI
@@ -475,6 +583,8 @@ void qb_shutdown(void) {
     cudaFree(d->d_chunk_min);
     cudaFree(d->d_cand);
     cudaFree(d->d_cand_count);
+    cudaFree(d->d_batch_coeffs);
+    cudaFree(d->d_batch_out);
     cudaFreeHost(d->h_cand_count);
     cudaEventDestroy(d->ev0);
     cudaEventDestroy(d->ev1);
@@ -531,14 +641,12 @@ int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, con
 
 int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                    double* kernel_ms) {
-  (void)coeffs; (void)n; (void)count; (void)argmin_bits; (void)values; (void)kernel_ms;
-  return qb::fail(QB_E_INTERNAL, "qb_solve_batch: not built yet");
+  return qb::batch_impl(coeffs, n, count, argmin_bits, values, kernel_ms);
 }
 
 int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_t count, double* values,
                    double* fields) {
-  (void)coeffs; (void)n; (void)k; (void)c_begin; (void)count; (void)values; (void)fields;
-  return qb::fail(QB_E_INTERNAL, "qb_prefix_eval: not built yet");
+  return qb::prefix_impl(coeffs, n, k, c_begin, count, values, fields);
 }
 
 }  // extern "C"

@@ -119,7 +119,7 @@ __device__ __forceinline__ Rec shfl_rec(const Rec& r, int src) {
 
 // Block-wide argmin of Rec (warp shuffle -> shared memory -> warp 0).  Result valid in thread 0.
 template <int TPB>
-__device__ __forceinline__ Rec cta_reduce(Rec r) {
+__device__ __forceinline__ Rec cta_reduce(Rec r, int nwarps = TPB / 32) {
   __shared__ Rec sh[TPB / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -130,7 +130,7 @@ __device__ __forceinline__ Rec cta_reduce(Rec r) {
   if (lane == 0) sh[warp] = r;
   __syncthreads();
   if (warp == 0) {
-    r = (lane < TPB / 32) ? sh[lane] : Rec{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+    r = (lane < nwarps) ? sh[lane] : Rec{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       Rec o = shfl_rec(r, (lane + off) & 31);

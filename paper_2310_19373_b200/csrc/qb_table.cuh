@@ -221,6 +221,26 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
 }
 
+// Standalone chunk-start ("prefix") evaluation for the qb_prefix_eval test hook: runs the very
+// base_eval<B, L> the traversal uses and converts back to coefficient units (x 2^-e).
+template <int B1, int B2, int SB, int L>
+__global__ void prefix_eval_kernel(const __grid_constant__ TableParams p, double* vals, double* fields, int e) {
+  constexpr int B = B1 + B2;
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long c = p.chunk_begin + idx;
+  if (c >= p.chunk_end) return;
+  const unsigned long long s = chunk_prefix(p, c);
+  long long V;
+  float H[B], F[NF];
+  base_eval<B, L>(p, s << L, L, V, H, F);
+  vals[idx] = ldexp((double)V, -e);
+#pragma unroll
+  for (int i = 0; i < B; ++i) fields[idx * L + i] = ldexp((double)(H[i] + p.d[i]), -e);
+#pragma unroll
+  for (int m = 0; m < L - B; ++m) fields[idx * L + B + m] = ldexp((double)(F[m] + p.d[B + m]), -e);
+}
+
 // Single CTA: reduce the per-CTA records, then one warp re-evaluates the winning super-block and
 // picks the lowest-key minimiser inside it.  Writes p.final_out.
 template <int B1, int B2, int SB, int L>

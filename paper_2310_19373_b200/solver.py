@@ -165,6 +165,35 @@ def solve_parallel(instance: QuboInstance, config: SolveConfig | None = None) ->
     return _solution(instance, res, (1 << instance.n) - (1 << m), t0)
 
 
+def solve_batch(instances) -> list[Solution]:
+    """Solve many independent instances of one size n <= 24 in one GPU launch (one CTA per
+    instance).  Each result equals ``solve_incremental`` of that instance (same tie rule).
+    The reference has no batch entry point; its equivalent is a loop / thread pool of
+    solve_incremental calls."""
+    if isinstance(instances, np.ndarray):
+        coeffs = np.ascontiguousarray(instances, dtype=np.float64)
+        if coeffs.ndim != 3 or coeffs.shape[1] != coeffs.shape[2]:
+            raise ValueError(f"batch must have shape (count, n, n), got {coeffs.shape}")
+        insts = None
+    else:
+        insts = list(instances)
+        if not insts:
+            return []
+        n0 = insts[0].n
+        if any(i.n != n0 for i in insts):
+            raise ValueError("all instances of a batch must have the same n")
+        coeffs = np.stack([i.coeffs for i in insts])
+    count, n = coeffs.shape[0], coeffs.shape[1]
+    if insts is None:  # normalise like QuboInstance (fold the lower triangle, validate)
+        insts = [QuboInstance(coeffs[b]) for b in range(count)]
+        coeffs = np.stack([i.coeffs for i in insts])
+    t0 = time.perf_counter()
+    bits, vals, _ = _lib.solve_batch(coeffs)
+    elapsed = max(time.perf_counter() - t0, 1e-9)
+    return [Solution(minimizer=bits_from_int(int(bits[b]), n), value=float(vals[b]), evaluations=(1 << n) - 1,
+                     elapsed=elapsed) for b in range(count)]
+
+
 def solve(instance: QuboInstance, config: SolveConfig | None = None) -> Solution:
     """Dispatch on ``config.mode`` (solver.py:232-240)."""
     if config is None:

@@ -154,3 +154,48 @@ def test_config_e_n40_properties():
     for s in rng.integers(0, 1 << m, size=4):
         _, v, _ = O.solve_subspaces(c, m, int(s), int(s) + 1, threads=8)
         assert v >= sol.value
+
+
+def test_batch_config_c_golden(golden):
+    cb = golden["configC"]
+    batch = instances.config_batch(cb["count"], cb["n"])
+    bits, vals, ms = _lib.solve_batch(batch)
+    assert [int(b) for b in bits] == cb["bits"]
+    assert vals.tolist() == cb["values"]
+    sols = qb.solve_batch(batch[:64])
+    assert [_bits(s) for s in sols] == cb["bits"][:64]
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 9, 10, 11, 13, 16, 20])
+def test_batch_ties_and_sizes(n):
+    count = 40
+    batch = np.stack([_tie_heavy(n, 77 * n + b, -1, 1) for b in range(count)])
+    batch[3] = 0.0  # all states tied: candidate overflow -> single-instance fallback
+    bits, vals, _ = _lib.solve_batch(batch)
+    for b in range(count):
+        want, wv, _ = O.expected_argmin(batch[b], 0)
+        assert int(bits[b]) == want, (n, b)
+        assert vals[b] == wv
+
+
+def test_batch_float_instances_vs_oracle():
+    for n in (12, 18):
+        batch = np.stack([instances.normal_coeffs(n, 5000 + b) for b in range(24)])
+        bits, vals, _ = _lib.solve_batch(batch)
+        ob, ov = O.solve_batch(batch, threads=8)
+        assert [int(b) for b in bits] == [int(b) for b in ob]
+        assert vals.tolist() == ov.tolist()
+
+
+@pytest.mark.parametrize("n,k", [(24, 14), (30, 14), (22, 12), (18, 9)])
+def test_prefix_eval_hook(n, k):
+    c = instances.config_coeffs("D", 2, n=n)
+    L = n - k
+    count = min(1 << k, 300)
+    vals, fields = _lib.prefix_eval(c, k, 0, count)
+    sym = np.triu(c, 1) + np.triu(c, 1).T
+    for idx in range(0, count, 7):
+        x = np.array([(idx << L >> i) & 1 for i in range(n)], dtype=np.float64)
+        assert vals[idx] == O.eval_upper(c, x)
+        want = np.diag(c)[:L] + sym[:L] @ x
+        assert np.array_equal(fields[idx], want), (n, k, idx)
