@@ -69,15 +69,22 @@ struct KernelSet {
 #define QB_BIG_B1 5
 #define QB_BIG_B2 5
 #endif
-constexpr int BIG_B1 = QB_BIG_B1, BIG_B2 = QB_BIG_B2, BIG_SB = 0, BIG_BE = BIG_B1 + BIG_B2 + BIG_SB;
+#ifndef QB_BIG_SB
+#define QB_BIG_SB 0
+#endif
+constexpr int BIG_B1 = QB_BIG_B1, BIG_B2 = QB_BIG_B2, BIG_SB = QB_BIG_SB, BIG_BE = BIG_B1 + BIG_B2 + BIG_SB;
 static KernelSet g_sets[] = {
     QB_KS(0, 1, 0, 1),  QB_KS(1, 1, 0, 2),  QB_KS(1, 2, 0, 3),  QB_KS(2, 2, 0, 4),  QB_KS(2, 3, 0, 5),
     QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KS(5, 5, 0, 10),
-#if QB_BIG_B1 + QB_BIG_B2 != 10
-    QB_KS(BIG_B1, BIG_B2, 0, BIG_BE),
+#if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB != 10
+    QB_KS(BIG_B1, BIG_B2, BIG_SB, BIG_BE),
 #endif
-    QB_KS(BIG_B1, BIG_B2, 0, 12), QB_KS(BIG_B1, BIG_B2, 0, 14), QB_KS(BIG_B1, BIG_B2, 0, 16),
-    QB_KS(BIG_B1, BIG_B2, 0, 18), QB_KS(BIG_B1, BIG_B2, 0, 20), QB_KS(BIG_B1, BIG_B2, 0, 22),
+#if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB < 11
+    QB_KS(BIG_B1, BIG_B2, BIG_SB, 11),
+#endif
+    QB_KS(BIG_B1, BIG_B2, BIG_SB, 12), QB_KS(BIG_B1, BIG_B2, BIG_SB, 13),
+    QB_KS(BIG_B1, BIG_B2, BIG_SB, 14), QB_KS(BIG_B1, BIG_B2, BIG_SB, 16),
+    QB_KS(BIG_B1, BIG_B2, BIG_SB, 18), QB_KS(BIG_B1, BIG_B2, BIG_SB, 20), QB_KS(BIG_B1, BIG_B2, BIG_SB, 22),
 };
 
 static KernelSet* find_set(int BE, int L) {
@@ -102,6 +109,7 @@ struct Device {
   unsigned long long* d_cand_count = nullptr;
   unsigned long long* h_cand_count = nullptr;  // pinned
   size_t cand_cap = 0;
+  unsigned long long* d_work = nullptr;
   double* d_batch_coeffs = nullptr;
   size_t batch_coeffs_cap = 0;
   BatchOut* d_batch_out = nullptr;
@@ -129,6 +137,7 @@ static int get_device(Device** out) {
     QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
     QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
     QB_CUDA(cudaMalloc(&d->d_cand_count, sizeof(unsigned long long)));
+    QB_CUDA(cudaMalloc(&d->d_work, sizeof(unsigned long long)));
     QB_CUDA(cudaMallocHost(&d->h_cand_count, sizeof(unsigned long long)));
     g_devs[dev] = std::move(d);
   }
@@ -241,13 +250,13 @@ static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int
     return QB_OK;
   }
   BE = BIG_BE;
-  // enough chunks for ~64 grid-stride rounds of resident threads on every shard
-  const double want_chunks = 64.0 * sms * 4 * TPB * (double)shard_count;
+  // ~16 chunks per resident thread on every shard (dynamic scheduling keeps the tail to one chunk)
+  const double want_chunks = 16.0 * sms * QB_MINB * TPB * (double)shard_count;
   int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
   int Lw = n - want_k;
   Lw = std::max(Lw, BIG_BE);
   Lw = std::min(Lw, std::min(22, lmax));
-  if (Lw > 12) Lw = 2 * (Lw / 2);
+  if (Lw > 14) Lw = 2 * (Lw / 2);
   L = Lw;
   return QB_OK;
 }
@@ -357,6 +366,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   if (int rc = ensure(&dev->d_cta, &dev->cta_cap, (size_t)grid)) return rc;
   P.cta_out = dev->d_cta;
   P.final_out = dev->d_final;
+  P.work = dev->d_work;
   P.nrec = grid;
   P.mode = pl.exact ? MODE_SEARCH : MODE_SEARCH_RECORD;
   if (!pl.exact) {
@@ -370,6 +380,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
 
   cudaStream_t st = dev->stream;
+  QB_CUDA(cudaMemsetAsync(dev->d_work, 0, sizeof(unsigned long long), st));
   QB_CUDA(cudaEventRecord(dev->ev0, st));
   ks.search<<<grid, TPB, 0, st>>>(P);
   QB_CUDA(cudaGetLastError());
@@ -583,6 +594,7 @@ void qb_shutdown(void) {
     cudaFree(d->d_chunk_min);
     cudaFree(d->d_cand);
     cudaFree(d->d_cand_count);
+    cudaFree(d->d_work);
     cudaFree(d->d_batch_coeffs);
     cudaFree(d->d_batch_out);
     cudaFreeHost(d->h_cand_count);

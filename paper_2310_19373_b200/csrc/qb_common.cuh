@@ -54,6 +54,7 @@ struct alignas(16) TableParams {
   unsigned long long cand_cap;
   Rec* cta_out;                    // one record per CTA
   FinalOut* final_out;
+  unsigned long long* work;        // dynamic chunk counter (zeroed before each search launch)
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };

@@ -85,7 +85,7 @@ __host__ __device__ constexpr int ctz_c(int k) { return (k & 1) ? 0 : 1 + ctz_c(
 // Per state: half an FADD2 (two states, T pair from the constant bank through uniform
 // registers), half an FMNMX3, and 1/(2P) of an LDCU.128.
 template <int B1, int B2, int SB, int NF>
-__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
+__device__ __forceinline__ float block_min_p1(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
   constexpr int B = B1 + B2, NU = 1 << B1, NW = 1 << B2, P = 1 << SB;
   static_assert(B2 >= 1, "inner low part needs at least one bit");
   float rmin = 0.f;
@@ -143,6 +143,83 @@ __device__ __forceinline__ float block_min(const TableParams& p, const float (&H
   return rmin;
 }
 
+// SB >= 1: P = 2^SB sub-blocks share every T load.  To keep registers low the u rows are
+// visited in Gray order and each sub-block's A_u is one running register (one FADD per
+// u-step), so only P x 2^B2 Bw values and P x B1 high fields stay live.
+template <int B1, int B2, int SB, int NF>
+__device__ __forceinline__ float block_min_shared(const TableParams& p, const float (&H)[B1 + B2],
+                                                  const float (&F)[NF]) {
+  constexpr int B = B1 + B2, NU = 1 << B1, NW = 1 << B2, P = 1 << SB;
+  static_assert(B2 >= 2 && (P % 2) == 0, "shared-table variant needs B2 >= 2 and an even sub-block count");
+  float Bw[P][NW];
+  float Hh[P][B1 > 0 ? B1 : 1];
+  float A[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    float hs[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      float h = H[i];
+#pragma unroll
+      for (int t = 0; t < SB; ++t)
+        if ((s >> t) & 1) h += p.Qs[i][B + t];
+      hs[i] = h;
+    }
+    float dl = 0.f;
+#pragma unroll
+    for (int t = 0; t < SB; ++t) {
+      if (!((s >> t) & 1)) continue;
+      dl += p.d[B + t] + F[t];
+#pragma unroll
+      for (int t2 = t + 1; t2 < SB; ++t2)
+        if ((s >> t2) & 1) dl += p.Qs[B + t][B + t2];
+    }
+    Bw[s][0] = 0.f;
+#pragma unroll
+    for (int i = 0; i < B2; ++i)
+#pragma unroll
+      for (int w = 0; w < (1 << i); ++w) Bw[s][w + (1 << i)] = Bw[s][w] + hs[i];
+#pragma unroll
+    for (int i = 0; i < B1; ++i) Hh[s][i] = hs[B2 + i];
+    A[s] = dl;
+  }
+  float rmin = 0.f;
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    const int u = k ^ (k >> 1);
+    if (k > 0) {
+      const int i = ctz_c(k);
+      const bool up = (u >> i) & 1;
+#pragma unroll
+      for (int s = 0; s < P; ++s) A[s] = up ? (A[s] + Hh[s][i]) : (A[s] - Hh[s][i]);
+    }
+    float acc[P];
+#pragma unroll
+    for (int w = 0; w < NW; w += 4) {
+      const float4 t4 = *reinterpret_cast<const float4*>(&p.T[u * NW + w]);
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const float2 c0 = add_f32x2(make_float2(Bw[s][w], Bw[s][w + 1]), make_float2(t4.x, t4.y));
+        const float2 c1 = add_f32x2(make_float2(Bw[s][w + 2], Bw[s][w + 3]), make_float2(t4.z, t4.w));
+        acc[s] = (w == 0) ? fminf(c0.x, c0.y) : fminf(fminf(acc[s], c0.x), c0.y);
+        acc[s] = fminf(fminf(acc[s], c1.x), c1.y);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < P; s += 2) {
+      const float r0 = acc[s] + A[s], r1 = acc[s + 1] + A[s + 1];
+      rmin = (k == 0 && s == 0) ? fminf(r0, r1) : fminf(fminf(rmin, r0), r1);
+    }
+  }
+  return rmin;
+}
+
+template <int B1, int B2, int SB, int NF>
+__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
+  if constexpr (SB == 0) return block_min_p1<B1, B2, SB, NF>(p, H, F);
+  else return block_min_shared<B1, B2, SB, NF>(p, H, F);
+}
+
 // Every state of super-block j of chunk prefix s, evaluated directly from its base (finalize and
 // collect; rare).  Calls fn(z_block, value) for the 2^(B+SB) states, z_block = (sub << B) | z.
 template <int B, int SB, int L, class Fn>
@@ -185,10 +262,29 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
   constexpr int NF = (L - B) > 0 ? (L - B) : 1;
   static_assert(LO >= 0, "block bits exceed chunk bits");
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+  const int lane = threadIdx.x & 31;
+  // Work distribution: the search pass hands out 32 consecutive chunks per warp from a global
+  // counter (one atomic per 32 chunks) so all SMs finish within one chunk of each other; the
+  // collect pass (few chunks survive its filter) is a plain grid-stride loop.
+  unsigned long long next = (unsigned long long)blockIdx.x * TPB + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * TPB;
-  for (unsigned long long c = p.chunk_begin + (unsigned long long)blockIdx.x * TPB + threadIdx.x; c < p.chunk_end;
-       c += stride) {
-    if (COLLECT && p.chunk_min[c - p.chunk_begin] > p.theta) continue;
+  for (;;) {
+    unsigned long long ci;
+    if (COLLECT) {
+      ci = next;
+      next += stride;
+      if (ci >= nchunks) break;
+    } else {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(p.work, 32ull);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= nchunks) break;
+      ci = base + lane;
+      if (ci >= nchunks) continue;
+    }
+    const unsigned long long c = p.chunk_begin + ci;
+    if (COLLECT && p.chunk_min[ci] > p.theta) continue;
     const unsigned long long s = chunk_prefix(p, c);
     long long V;
     float H[B], F[NF];
@@ -214,7 +310,7 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
         if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
       }
     }
-    if (!COLLECT && p.mode == MODE_SEARCH_RECORD) p.chunk_min[c - p.chunk_begin] = cmin;
+    if (!COLLECT && p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
   if (COLLECT) return;
   const Rec r = cta_reduce<TPB>(best);
