@@ -45,7 +45,7 @@ CONFIG_DESC = {
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
 # SASS instructions per state of the table kernel's inner block (cuobjdump count)
-SASS_INSTR_PER_STATE = 1.27
+SASS_INSTR_PER_STATE = 1.52  # ncu smsp__inst_executed x 32 / 2^40 (profiles/r01_ncu_search_summary.txt)
 
 
 def parse():
@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the informational A-D config lines")
     return ap.parse_args()
 
 
@@ -156,6 +157,47 @@ def cpu_sample(coeffs, seconds: float):
             "sample": f"{count} of {1 << m} m={m} subspaces ({states:.3g} states, {dt:.1f} s) of config E via "
                       f"oracle/gray_oracle.c oc_solve_subspaces (reference solve_parallel restated), {threads} threads",
             "seconds": dt}
+
+
+def extra_configs(qb, _lib, instances, reps: int = 5):
+    """Informational per-config throughput (rank 0, N=1): BASELINE configs A-D besides the
+    headline E.  kernel = device time of the solve launches (library CUDA events); e2e = the
+    public API call with host buffers (planning, H2D, kernels, D2H)."""
+    import numpy as np
+
+    out = {}
+    for name in ("A", "B", "D"):
+        c = instances.config_coeffs(name, 0)
+        inst = qb.QuboInstance(c)
+        n = inst.n
+        for _ in range(2):
+            qb.solve_incremental(inst)
+        ks, es = [], []
+        for _ in range(reps):
+            r = _lib.solve(inst.coeffs)
+            ks.append(r.kernel_ms)
+            t0 = time.perf_counter()
+            qb.solve_incremental(inst)
+            es.append(time.perf_counter() - t0)
+        km, em = float(np.median(ks)), float(np.median(es))
+        out[name] = {"n": n, "kernel_ms": km, "states_per_s": 2 ** n / (km * 1e-3), "e2e_ms": em * 1e3,
+                     "e2e_states_per_s": 2 ** n / em, "exact_path": bool(r.exact)}
+    batch = instances.config_batch(4096, 16)
+    for _ in range(2):
+        _lib.solve_batch(batch)
+    ks, es = [], []
+    for _ in range(reps):
+        _, _, km = _lib.solve_batch(batch)
+        ks.append(km)
+        t0 = time.perf_counter()
+        qb.solve_batch(batch, as_arrays=True)
+        es.append(time.perf_counter() - t0)
+    km, em = float(np.median(ks)), float(np.median(es))
+    states = 4096 * 2 ** 16
+    out["C"] = {"n": 16, "instances": 4096, "kernel_ms": km, "states_per_s": states / (km * 1e-3),
+                "e2e_ms": em * 1e3, "e2e_states_per_s": states / em,
+                "h2d_bytes": int(batch.nbytes)}
+    return out
 
 
 def run_reference(args, world, rank):
@@ -302,6 +344,8 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if rank == 0 and world == 1 and not args.no_extra:
+        line["configs"] = extra_configs(qb, _lib, instances)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_sample(inst.coeffs, args.cpu_seconds)
         cb.pop("seconds", None)

@@ -93,6 +93,15 @@ double qb_eval_upper(const double* coeffs, int n, const double* x);
 int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule,
              uint32_t shard, uint32_t shard_count, int variant, qb_result* out);
 
+/* Every minimiser of the subspace {x : x >> (n - m_fix) == suffix} (BASELINE config A: "min
+ * value + all minimising vectors"; the reference returns one, SPEC.md:273 lists this as a
+ * non-goal).  Sorted by the Gray tie rule m_tie, so out[0] is what qb_solve returns.  Writes up
+ * to `cap` minimisers; *count receives the total number (which may exceed cap), *value the
+ * minimum (eval_upper).  Exact on the integer path; on the float path the candidates within the
+ * quantization bound are re-evaluated with eval_upper and those equal to the minimum kept. */
+int qb_all_minimisers(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, uint64_t* out,
+                      uint64_t cap, uint64_t* count, double* value);
+
 /* Seam 1: the reference operator _kernels.gray_scan(coeffs, qua, lin, x0, v0, n_free)
  * (_kernels.py:46-75) with its exact return contract: x_min (fp64[n], 0/1), v_min
  * (eval_upper(x_min), or v0 when no visited state beats the start), steps = 2^n_free - 1.
@@ -102,8 +111,9 @@ int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, con
                  int n, int n_free, double* x_min, double* v_min, uint64_t* steps);
 
 /* Batch of independent instances (BASELINE config C): `count` instances of size n (n <= 24),
- * coeffs laid out [count][n][n]; instance b is solved like solve_incremental (global Gray-rank
- * tie rule).  One CTA per instance, T table in shared memory.  The reference has no batch API:
+ * coeffs laid out [count][n][n]; entries below the diagonal are folded into the upper triangle
+ * (QuboInstance convention, core.py:66-72).  Instance b is solved like solve_incremental (global
+ * Gray-rank tie rule); values[b] = eval_upper(argmin) of the folded matrix.  One CTA per instance, T table in shared memory.  The reference has no batch API:
  * this replaces a loop / thread pool of solve_incremental calls (solver.py:118-136). */
 int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                    double* kernel_ms);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "qb_eval_upper": (ctypes.c_double, [_dp, ctypes.c_int, _dp]),
     "qb_solve": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(QbResult)]),
+    "qb_all_minimisers": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _u64p,
+                                         ctypes.c_uint64, _u64p, _dp]),
     "qb_gray_scan": (ctypes.c_int, [_dp, _dp, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _dp,
                                     _u64p]),
     "qb_solve_batch": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, _u64p, _dp, _dp]),
@@ -184,6 +186,20 @@ def solve(coeffs, m_fix: int = 0, suffix: int = 0, m_tie: int = 0, tie_rule: int
                         ctypes.byref(out))
     check(rc, "qb_solve")
     return out
+
+
+def all_minimisers(coeffs, m_fix: int = 0, suffix: int = 0, m_tie: int = 0, cap: int = 1 << 20,
+                   device: int | None = None):
+    """(value, uint64 array of every minimiser sorted by the Gray tie rule, total count)."""
+    c = _f64(coeffs)
+    init(device)
+    out = np.zeros(max(cap, 1), dtype=np.uint64)
+    cnt = ctypes.c_uint64()
+    val = ctypes.c_double()
+    rc = lib().qb_all_minimisers(_ptr(c), c.shape[0], m_fix, suffix, m_tie, out.ctypes.data_as(_u64p), cap,
+                                 ctypes.byref(cnt), ctypes.byref(val))
+    check(rc, "qb_all_minimisers")
+    return val.value, out[: min(cap, cnt.value)].copy(), int(cnt.value)
 
 
 def gray_scan(coeffs, qua, lin, x0, v0, n_free, device: int | None = None):

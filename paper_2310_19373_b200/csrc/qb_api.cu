@@ -291,7 +291,8 @@ static double eval_bits(const double* c, int n, unsigned long long x) {
 
 // ------------------------------------------------------------------ the solve
 static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long suffix, int m_tie, int rule,
-                      uint32_t shard, uint32_t shard_count, int variant, qb_result* out) {
+                      uint32_t shard, uint32_t shard_count, int variant, qb_result* out,
+                      std::vector<unsigned long long>* all_out = nullptr) {
   auto t_start = std::chrono::steady_clock::now();
   if (!coeffs || !out) return fail(QB_E_ARG, "null pointer");
   if (n < 1) return fail(QB_E_ARG, "dimension must be at least 1");
@@ -368,8 +369,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   P.final_out = dev->d_final;
   P.work = dev->d_work;
   P.nrec = grid;
-  P.mode = pl.exact ? MODE_SEARCH : MODE_SEARCH_RECORD;
-  if (!pl.exact) {
+  const bool collect = !pl.exact || all_out != nullptr;
+  P.mode = collect ? MODE_SEARCH_RECORD : MODE_SEARCH;
+  if (collect) {
     if (nchunks > (1ull << 27)) return fail(QB_E_INTERNAL, "too many chunks for the approximate path");
     if (int rc = ensure(&dev->d_chunk_min, &dev->chunk_min_cap, (size_t)nchunks)) return rc;
     P.chunk_min = dev->d_chunk_min;
@@ -400,7 +402,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const FinalOut fo = *dev->h_final;
   if (!fo.found) return fail(QB_E_INTERNAL, "finalize found no state attaining the block minimum");
 
-  if (pl.exact) {
+  if (!collect) {
     out->argmin_bits = fo.x;
     out->tie_key = fo.key;
     out->value_key = (unsigned long long)fo.val ^ (1ull << 63);
@@ -423,8 +425,22 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     out->kernel_ms += ms;
     out->collect_ms = ms;
     out->launches += 1;
-    const unsigned long long cnt = *dev->h_cand_count;
+    unsigned long long cnt = *dev->h_cand_count;
     if (cnt == 0) return fail(QB_E_INTERNAL, "collect pass found no candidate");
+    if (cnt > P.cand_cap && all_out != nullptr && cnt <= (1ull << 27)) {
+      // all-minimisers request with more ties than the buffer holds: grow it and collect again
+      if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)cnt)) return rc;
+      P.cand = dev->d_cand;
+      P.cand_cap = dev->cand_cap;
+      QB_CUDA(cudaMemsetAsync(dev->d_cand_count, 0, sizeof(unsigned long long), st));
+      ks.collect<<<grid, TPB, 0, st>>>(P);
+      QB_CUDA(cudaGetLastError());
+      out->launches += 1;
+      QB_CUDA(cudaMemcpyAsync(dev->h_cand_count, dev->d_cand_count, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+      QB_CUDA(cudaStreamSynchronize(st));
+      cnt = *dev->h_cand_count;
+    }
     if (cnt > P.cand_cap)
       return fail(QB_E_INTERNAL, "more than " + std::to_string(P.cand_cap) + " near-tied minimisers (float path)");
     std::vector<unsigned long long> cand(cnt);
@@ -433,16 +449,28 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     double bv = 0.0;
     unsigned long long bx = 0, bk = ~0ull;
     bool have = false;
-    for (unsigned long long x : cand) {
-      const double v = eval_bits(coeffs, n, x);
+    std::vector<double> cv(cand.size());
+    for (size_t t = 0; t < cand.size(); ++t) {
+      const unsigned long long x = cand[t];
+      const double v = cv[t] = pl.exact ? (double)0 : eval_bits(coeffs, n, x);
       const unsigned long long key = host_tie_key(x, n, m_tie, rule);
       if (!have || v < bv || (v == bv && key < bk)) { bv = v; bx = x; bk = key; have = true; }
+    }
+    if (pl.exact) bv = eval_bits(coeffs, n, bx);  // exact path: all candidates share the minimum
+    if (all_out) {
+      // every candidate attaining the minimum, ordered by the tie rule (element 0 = the argmin)
+      std::vector<std::pair<unsigned long long, unsigned long long>> keyed;
+      for (size_t t = 0; t < cand.size(); ++t)
+        if (pl.exact || cv[t] == bv) keyed.emplace_back(host_tie_key(cand[t], n, m_tie, rule), cand[t]);
+      std::sort(keyed.begin(), keyed.end());
+      all_out->clear();
+      for (auto& kx : keyed) all_out->push_back(kx.second);
     }
     out->candidates = cnt;
     out->argmin_bits = bx;
     out->tie_key = bk;
     out->value = bv;
-    out->value_key = ordered_double(bv);
+    out->value_key = pl.exact ? ((unsigned long long)fo.val ^ (1ull << 63)) : ordered_double(bv);
   }
   out->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return QB_OK;
@@ -540,9 +568,14 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
     }
   }
   // instances with more than BATCH_CAP near-tied minimisers: full single-instance path
+  std::vector<double> up((size_t)n * n);
   for (uint64_t b : fallback) {
+    const double* c = coeffs + b * (uint64_t)n * n;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        up[(size_t)i * n + j] = j < i ? 0.0 : (j == i ? c[i * n + i] : c[i * n + j] + c[j * n + i]);
     qb_result r;
-    if (int rc = solve_impl(coeffs + b * (uint64_t)n * n, n, 0, 0, 0, RULE_GRAY, 0, 1, QB_VARIANT_AUTO, &r)) return rc;
+    if (int rc = solve_impl(up.data(), n, 0, 0, 0, RULE_GRAY, 0, 1, QB_VARIANT_AUTO, &r)) return rc;
     argmin_bits[b] = r.argmin_bits;
     values[b] = r.value;
   }
@@ -611,6 +644,20 @@ double qb_eval_upper(const double* coeffs, int n, const double* x) { return qb::
 int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule, uint32_t shard,
              uint32_t shard_count, int variant, qb_result* out) {
   return qb::solve_impl(coeffs, n, m_fix, suffix, m_tie, tie_rule, shard, shard_count, variant, out);
+}
+
+int qb_all_minimisers(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, uint64_t* out,
+                      uint64_t cap, uint64_t* count, double* value) {
+  if (!out && cap) return qb::fail(QB_E_ARG, "null output buffer");
+  if (!count || !value) return qb::fail(QB_E_ARG, "null pointer");
+  std::vector<unsigned long long> all;
+  qb_result r;
+  int rc = qb::solve_impl(coeffs, n, m_fix, suffix, m_tie, qb::RULE_GRAY, 0, 1, QB_VARIANT_AUTO, &r, &all);
+  if (rc) return rc;
+  *count = all.size();
+  *value = r.value;
+  for (uint64_t t = 0; t < cap && t < all.size(); ++t) out[t] = all[t];
+  return QB_OK;
 }
 
 int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, const double* x0, double v0, int n,

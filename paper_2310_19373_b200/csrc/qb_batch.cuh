@@ -33,7 +33,7 @@ struct BatchOut {
 };
 
 struct BatchParams {
-  const double* coeffs;  // [count][n][n] upper-triangular fp64
+  const double* coeffs;  // [count][n][n] fp64; entries below the diagonal are folded in
   BatchOut* out;         // [count]
   int n;
   int count;
@@ -41,9 +41,22 @@ struct BatchParams {
 
 __device__ __forceinline__ float2 batch_add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
-// min over the 2^B states of one block, table from shared memory (broadcast LDS.128)
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 lds64(unsigned addr) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
+// min over the 2^B states of one block, table from shared memory (broadcast LDS.128).  sT is a
+// shared-space byte address made opaque by the caller each iteration, so ptxas cannot hoist all
+// 2^B table loads out of the chunk loop into (spilled) registers.
 template <int B1, int B2>
-__device__ __forceinline__ float batch_block_min(const float* __restrict__ sT, const float (&H)[B1 + B2]) {
+__device__ __forceinline__ float batch_block_min(unsigned sT, const float (&H)[B1 + B2]) {
   constexpr int NU = 1 << B1, NW = 1 << B2;
   float Bw[NW];
   Bw[0] = 0.f;
@@ -64,14 +77,14 @@ __device__ __forceinline__ float batch_block_min(const float* __restrict__ sT, c
     if constexpr (NW >= 4) {
 #pragma unroll
       for (int w = 0; w < NW; w += 4) {
-        const float4 t4 = *reinterpret_cast<const float4*>(&sT[u * NW + w]);
+        const float4 t4 = lds128(sT + 4u * (u * NW + w));
         const float2 c0 = batch_add2(make_float2(Bw[w], Bw[w + 1]), make_float2(t4.x, t4.y));
         const float2 c1 = batch_add2(make_float2(Bw[w + 2], Bw[w + 3]), make_float2(t4.z, t4.w));
         acc = (w == 0) ? fminf(c0.x, c0.y) : fminf(fminf(acc, c0.x), c0.y);
         acc = fminf(fminf(acc, c1.x), c1.y);
       }
     } else {
-      const float2 t = *reinterpret_cast<const float2*>(&sT[u * NW]);
+      const float2 t = lds64(sT + 4u * (u * NW));
       const float2 c = batch_add2(make_float2(Bw[0], Bw[1]), t);
       acc = fminf(c.x, c.y);
     }
@@ -102,38 +115,45 @@ template <int B1, int B2>
 __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams bp) {
   constexpr int B = B1 + B2;
   constexpr int NT = 1 << B;
-  __shared__ float sQ[BATCH_NMAX][BATCH_NMAX + 1];  // quantized: diagonal on the diagonal, symmetric off
+  constexpr int CHUNK_CAP = 32;
+  __shared__ double sC[BATCH_NMAX][BATCH_NMAX + 1];  // folded fp64 coefficients, symmetric copy
+  __shared__ float sQ[BATCH_NMAX][BATCH_NMAX + 1];   // quantized: diagonal on the diagonal, symmetric off
   __shared__ __align__(16) float sT[NT];
   __shared__ double sred[BATCH_TPB_MAX / 32];
-  __shared__ int sflag[3];                          // [0]: not-integral, [1]: not-exact, [2]: bound violated
+  __shared__ int sflag[2];                           // [0]: not integral, [1]: not exact
   __shared__ unsigned long long scand[BATCH_CAP];
-  __shared__ int scount;
+  __shared__ unsigned int schunk[CHUNK_CAP];
+  __shared__ int scount, schunks;
   __shared__ Rec sbest;
   const int n = bp.n;
   const int tid = threadIdx.x, nth = blockDim.x;
   const double* C = bp.coeffs + (size_t)blockIdx.x * n * n;
   const int lane = tid & 31, warp = tid >> 5;
 
-  // ---- 1. quantization: bound M = max(r_in, max row abs sum), as in qb_api.cu quantize()
-  if (tid == 0) { sflag[0] = sflag[1] = sflag[2] = 0; scount = 0; }
+  // ---- 0. fold (QuboInstance convention, core.py:66-72) into shared memory: one pass over global
+  if (tid == 0) { sflag[0] = sflag[1] = 0; scount = 0; schunks = 0; }
+  for (int idx = tid; idx < n * n; idx += nth) {
+    const int i = idx / n, j = idx % n;
+    if (j < i) continue;
+    const double v = (i == j) ? C[idx] : __dadd_rn(C[idx], C[j * n + i]);
+    sC[i][j] = v;
+    sC[j][i] = v;
+  }
   __syncthreads();
-  auto csym = [&](int i, int j) -> double { return i <= j ? C[i * n + j] : C[j * n + i]; };
+
+  // ---- 1. quantization: bound M = max(r_in, max row abs sum), as in qb_api.cu quantize()
   double part_rin = 0.0, part_row = 0.0;
   int nnz = 0;
   for (int idx = tid; idx < n * n; idx += nth) {
     const int i = idx / n, j = idx % n;
-    if (j >= i) {
-      const double v = C[i * n + j];
-      if (v != 0.0) ++nnz;
-      if (floor(v) != v) sflag[0] = 1;
-      if (i < B) part_rin += fabs(v);  // r_in: every upper entry in a row of the block bits
-    }
+    if (j < i) continue;
+    const double v = sC[i][j];
+    if (v != 0.0) ++nnz;
+    if (floor(v) != v) sflag[0] = 1;
+    if (i < B) part_rin += fabs(v);  // r_in: every upper entry in a row of the block bits
   }
-  // row abs sums: thread r < n computes row r
   if (tid < n) {
-    double ra = 0.0;
-    for (int j = 0; j < n; ++j) ra += fabs(csym(tid, j));
-    part_row = ra;
+    for (int j = 0; j < n; ++j) part_row += fabs(sC[tid][j]);
   }
   auto block_sum = [&](double v) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -160,44 +180,39 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   const double LIM = 16777215.0;
   int e = 0;
   if (!(M == 0.0 || (sflag[0] == 0 && M <= LIM))) e = (int)floor(log2(LIM / M));
-  // quantize (retry with e-1 if rounding pushed a sum over the bound)
-  for (int guard = 0; guard < 8; ++guard) {
+  for (int guard = 0; guard < 8; ++guard) {  // retry with e-1 if rounding pushed a sum over the bound
     double prin = 0.0, prow = 0.0;
     for (int idx = tid; idx < n * n; idx += nth) {
       const int i = idx / n, j = idx % n;
-      const double q = nearbyint(ldexp(csym(i, j), e));
+      const double q = nearbyint(ldexp(sC[i][j], e));
       sQ[i][j] = (float)q;
       if (j >= i && i < B) prin += fabs(q);
     }
     __syncthreads();
-    if (tid < n) {
-      double ra = 0.0;
-      for (int j = 0; j < n; ++j) ra += fabs((double)sQ[tid][j]);
-      prow = ra;
-    }
+    if (tid < n)
+      for (int j = 0; j < n; ++j) prow += fabs((double)sQ[tid][j]);
     const double ok_in = block_sum(prin), ok_row = block_max(prow);
     if (fmax(ok_in, ok_row) <= LIM) break;
     --e;
   }
   for (int idx = tid; idx < n * n; idx += nth) {
     const int i = idx / n, j = idx % n;
-    if (j >= i && ldexp(C[i * n + j], e) != (double)sQ[i][j]) sflag[1] = 1;
+    if (j >= i && ldexp(sC[i][j], e) != (double)sQ[i][j]) sflag[1] = 1;
   }
+  // ---- 2. inner table by doubling: T[z + 2^b] = T[z] + q_bb + sum_{i<b} z_i q_ib   (O(B) per entry)
+  if (tid == 0) sT[0] = 0.f;
   __syncthreads();
   const bool exact = sflag[1] == 0;
   const long long Eq = exact ? 0 : (long long)((nnz_all + 1.0) / 2.0) + 1;
-
-  // ---- 2. inner table T(z) = sum_{i<=j<B} q_ij z_i z_j
-  for (int z = tid; z < NT; z += nth) {
-    float t = 0.f;
-    for (int i = 0; i < B; ++i) {
-      if (!((z >> i) & 1)) continue;
-      for (int j = i; j < B; ++j)
-        if ((z >> j) & 1) t += sQ[i][j];
+#pragma unroll 1
+  for (int b = 0; b < B; ++b) {
+    for (int z = tid; z < (1 << b); z += nth) {
+      float t = sT[z] + sQ[b][b];
+      for (int i = 0; i < b; ++i) t = fmaf(((z >> i) & 1) ? 1.f : 0.f, sQ[i][b], t);
+      sT[z + (1 << b)] = t;
     }
-    sT[z] = t;
+    __syncthreads();
   }
-  __syncthreads();
 
   // ---- 3. search
   const int k = n - B;
@@ -208,32 +223,47 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
     long long V;
     float H[B];
     batch_base<B>(sQ, n, (unsigned long long)c << B, V, H);
-    const long long val = V + (long long)batch_block_min<B1, B2>(sT, H);
+    unsigned tp = (unsigned)__cvta_generic_to_shared(sT);
+    asm volatile("" : "+r"(tp));  // opaque per iteration: keeps ptxas from hoisting all 2^B table loads
+    const long long val = V + (long long)batch_block_min<B1, B2>(tp, H);
     tmin = min(tmin, val);
-    const unsigned long long K = ginv64(c);  // global Gray rank >> B (m_tie = 0, one block per chunk)
+    const unsigned long long K = ginv64(c);  // global Gray rank >> B (one block per chunk)
     if (val < best.val || (val == best.val && K < best.K)) best = Rec{val, K, c, 0u, 0u};
   }
   best = cta_reduce<BATCH_TPB_MAX>(best, (nth + 31) / 32);
   if (tid == 0) sbest = best;
   __syncthreads();
-  const long long vmin = sbest.val;
-  const long long theta = vmin + 2 * Eq;
+  const long long theta = sbest.val + 2 * Eq;
 
-  // ---- 4. candidates within 2*Eq of the quantized minimum
+  // ---- 4. certified candidates: list the chunks whose block minimum is <= theta, then the whole
+  //         CTA enumerates those blocks' states in parallel
   if (tmin <= theta) {
     for (unsigned int c = tid; c < chunks; c += nth) {
       long long V;
       float H[B];
       batch_base<B>(sQ, n, (unsigned long long)c << B, V, H);
-      if (V + (long long)batch_block_min<B1, B2>(sT, H) > theta) continue;
-      for (unsigned int z = 0; z < (unsigned int)NT; ++z) {
-        float r = sT[z];
-        for (int i = 0; i < B; ++i)
-          if ((z >> i) & 1u) r += H[i];
-        if (V + (long long)r <= theta) {
-          const int idx = atomicAdd(&scount, 1);
-          if (idx < BATCH_CAP) scand[idx] = ((unsigned long long)c << B) | z;
-        }
+      unsigned tp = (unsigned)__cvta_generic_to_shared(sT);
+      asm volatile("" : "+r"(tp));
+      if (V + (long long)batch_block_min<B1, B2>(tp, H) > theta) continue;
+      const int idx = atomicAdd(&schunks, 1);
+      if (idx < CHUNK_CAP) schunk[idx] = c;
+    }
+  }
+  __syncthreads();
+  const int nch = min(schunks, CHUNK_CAP);
+  for (int t = 0; t < nch; ++t) {
+    const unsigned int c = schunk[t];
+    long long V;
+    float H[B];
+    batch_base<B>(sQ, n, (unsigned long long)c << B, V, H);
+    for (unsigned int z = tid; z < (unsigned int)NT; z += nth) {
+      float r = sT[z];
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+        if ((z >> i) & 1u) r += H[i];
+      if (V + (long long)r <= theta) {
+        const int idx = atomicAdd(&scount, 1);
+        if (idx < BATCH_CAP) scand[idx] = ((unsigned long long)c << B) | z;
       }
     }
   }
@@ -243,7 +273,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   if (warp == 0) {
     const int cnt = scount;
     BatchOut o{0ull, 0.0, 0, cnt};
-    if (cnt > BATCH_CAP) {
+    if (cnt > BATCH_CAP || schunks > CHUNK_CAP) {
       o.status = 1;
     } else if (cnt == 0) {
       o.status = 2;
@@ -258,7 +288,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
           const double xi = (double)((x >> i) & 1ull);
           for (int j = i; j < n; ++j) {
             const double xj = (double)((x >> j) & 1ull);
-            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(C[i * n + j], xi), xj));
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sC[i][j], xi), xj));
           }
         }
         const unsigned long long key = ginv64(x);

@@ -165,33 +165,67 @@ def solve_parallel(instance: QuboInstance, config: SolveConfig | None = None) ->
     return _solution(instance, res, (1 << instance.n) - (1 << m), t0)
 
 
-def solve_batch(instances) -> list[Solution]:
+def _batch_coeffs(instances) -> np.ndarray:
+    """(count, n, n) fp64 upper-triangular coefficients, normalised like QuboInstance
+    (lower triangle folded, finiteness and cap checked), vectorised over the batch."""
+    if isinstance(instances, np.ndarray):
+        arr = np.asarray(instances, dtype=np.float64)
+        if arr.ndim != 3 or arr.shape[1] != arr.shape[2]:
+            raise ValueError(f"batch must have shape (count, n, n), got {arr.shape}")
+        n = arr.shape[1]
+        if n < 1:
+            raise ValueError("dimension must be at least 1")
+        if n > MAX_DIM:
+            raise DimensionCapError(f"dimension {n} exceeds cap {MAX_DIM}")
+        # the native batch path folds entries below the diagonal itself (QuboInstance
+        # convention) and rejects non-finite coefficients, so no numpy pass over the batch
+        arr = np.ascontiguousarray(arr)
+        return arr
+    insts = list(instances)
+    if not insts:
+        return np.zeros((0, 1, 1))
+    n0 = insts[0].n
+    if any(i.n != n0 for i in insts):
+        raise ValueError("all instances of a batch must have the same n")
+    return np.ascontiguousarray(np.stack([i.coeffs for i in insts]))
+
+
+def solve_batch(instances, *, as_arrays: bool = False):
     """Solve many independent instances of one size n <= 24 in one GPU launch (one CTA per
     instance).  Each result equals ``solve_incremental`` of that instance (same tie rule).
+    ``instances``: a sequence of QuboInstance or a (count, n, n) array.  Returns a list of
+    Solution, or with ``as_arrays=True`` the pair (minimizers uint8 (count, n), values (count,)).
     The reference has no batch entry point; its equivalent is a loop / thread pool of
     solve_incremental calls."""
-    if isinstance(instances, np.ndarray):
-        coeffs = np.ascontiguousarray(instances, dtype=np.float64)
-        if coeffs.ndim != 3 or coeffs.shape[1] != coeffs.shape[2]:
-            raise ValueError(f"batch must have shape (count, n, n), got {coeffs.shape}")
-        insts = None
-    else:
-        insts = list(instances)
-        if not insts:
-            return []
-        n0 = insts[0].n
-        if any(i.n != n0 for i in insts):
-            raise ValueError("all instances of a batch must have the same n")
-        coeffs = np.stack([i.coeffs for i in insts])
+    coeffs = _batch_coeffs(instances)
     count, n = coeffs.shape[0], coeffs.shape[1]
-    if insts is None:  # normalise like QuboInstance (fold the lower triangle, validate)
-        insts = [QuboInstance(coeffs[b]) for b in range(count)]
-        coeffs = np.stack([i.coeffs for i in insts])
+    if count == 0:
+        return (np.zeros((0, n), dtype=np.uint8), np.zeros(0)) if as_arrays else []
     t0 = time.perf_counter()
     bits, vals, _ = _lib.solve_batch(coeffs)
+    minimizers = ((bits[:, None] >> np.arange(n, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.uint8)
+    if as_arrays:
+        return minimizers, vals
     elapsed = max(time.perf_counter() - t0, 1e-9)
-    return [Solution(minimizer=bits_from_int(int(bits[b]), n), value=float(vals[b]), evaluations=(1 << n) - 1,
-                     elapsed=elapsed) for b in range(count)]
+    ev = (1 << n) - 1
+    return [Solution(minimizer=minimizers[b], value=float(vals[b]), evaluations=ev, elapsed=elapsed)
+            for b in range(count)]
+
+
+def all_minimizers(instance: QuboInstance, config: SolveConfig | None = None, *, max_count: int = 1 << 20):
+    """Minimum value and EVERY minimising vector (BASELINE config A), as a uint8 array of shape
+    (count, n) sorted by the tie rule of ``config`` (default: global Gray rank, so row 0 is
+    ``solve_incremental``'s minimiser; with ``mode="parallel"`` row 0 is ``solve_parallel``'s).
+    The reference returns a single minimiser (SPEC.md:273 non-goal); this is an extension.
+    Raises if more than ``max_count`` minimisers exist."""
+    if instance.n > MAX_DIM:
+        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+    m = _resolve_m(instance, config) if (config is not None and config.mode == "parallel") else 0
+    value, xs, count = _lib.all_minimisers(instance.coeffs, 0, 0, m, cap=max_count)
+    if count > max_count:
+        raise ValueError(f"{count} minimisers exceed max_count={max_count}")
+    bits = ((xs[:, None] >> np.arange(instance.n, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.uint8)
+    return float(value), bits
 
 
 def solve(instance: QuboInstance, config: SolveConfig | None = None) -> Solution:

@@ -199,3 +199,48 @@ def test_prefix_eval_hook(n, k):
         assert vals[idx] == O.eval_upper(c, x)
         want = np.diag(c)[:L] + sym[:L] @ x
         assert np.array_equal(fields[idx], want), (n, k, idx)
+
+
+@pytest.mark.parametrize("n", [3, 8, 12, 14])
+def test_all_minimizers_tie_heavy(n):
+    for rep in range(5):
+        c = _tie_heavy(n, 3100 * n + rep, -1, 1)
+        inst = qb.QuboInstance(c)
+        _, val, mins = O.expected_argmin(c, 0)
+        value, bits = qb.all_minimizers(inst)
+        got = [qb.bits_to_int(b) for b in bits]
+        assert got == [int(x) for x in mins], (n, rep)
+        assert value == val
+        # parallel tie rule ordering
+        m = n // 2
+        _, _, mins_m = O.expected_argmin(c, m)
+        _, bits_m = qb.all_minimizers(inst, qb.SolveConfig(threads=2, fixed_bits=m, mode="parallel"))
+        assert [qb.bits_to_int(b) for b in bits_m] == [int(x) for x in mins_m]
+
+
+def test_all_minimizers_config_a_and_floats():
+    c = instances.config_coeffs("A", 0)
+    _, val, mins = O.expected_argmin(c, 0)
+    value, bits = qb.all_minimizers(qb.QuboInstance(c))
+    assert [qb.bits_to_int(b) for b in bits] == [int(x) for x in mins] and value == val
+    z = np.zeros((14, 14))
+    value, bits = qb.all_minimizers(qb.QuboInstance(z))
+    assert len(bits) == 1 << 14 and qb.bits_to_int(bits[0]) == 0
+    c = instances.config_coeffs("B", 1, n=16)
+    _, val, mins = O.expected_argmin(c, 0)
+    value, bits = qb.all_minimizers(qb.QuboInstance(c))
+    assert [qb.bits_to_int(b) for b in bits] == [int(x) for x in mins]
+
+
+def test_batch_folds_lower_triangle_like_quboinstance():
+    rng = np.random.default_rng(11)
+    raw = rng.integers(-3, 4, size=(16, 9, 9)).astype(np.float64)  # full (non-triangular) matrices
+    mins, vals = qb.solve_batch(raw, as_arrays=True)
+    for b in range(16):
+        inst = qb.QuboInstance(raw[b])
+        sol = qb.solve_incremental(inst)
+        assert np.array_equal(mins[b], sol.minimizer) and vals[b] == sol.value
+    bad = raw.copy()
+    bad[5, 4, 2] = np.inf
+    with pytest.raises(ValueError):
+        qb.solve_batch(bad)
