@@ -346,6 +346,17 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_extra:
         line["configs"] = extra_configs(qb, _lib, instances)
+        # the literal per-step field-walk kernel (QB_VARIANT_FIELDWALK) on the same workload
+        _lib.solve(inst.coeffs, variant=_lib.VARIANT_FIELDWALK)
+        fw = _lib.solve(inst.coeffs, variant=_lib.VARIANT_FIELDWALK)
+        fw_states_s = states / (fw.search_ms * 1e-3)
+        line["variants"] = {
+            "table": {"search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s},
+            "fieldwalk": {"search_ms": fw.search_ms, "states_per_s": fw_states_s,
+                          "nominal_roofline_frac": fw_states_s * (n + 1) / peak,
+                          "same_argmin": int(fw.argmin_bits) == int(r.argmin_bits),
+                          "variant_used": int(fw.variant)},
+        }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_sample(inst.coeffs, args.cpu_seconds)
         cb.pop("seconds", None)

@@ -24,6 +24,7 @@
 #include "qb_common.cuh"
 #include "qb_table.cuh"
 #include "qb_batch.cuh"
+#include "qb_fieldwalk.cuh"
 
 namespace qb {
 
@@ -54,13 +55,20 @@ struct KernelSet {
   int B1, B2, SB, L;
   KFn search, collect, finalize;
   PFn prefix;
+  KFn fieldwalk;  // per-step field-walk search kernel with the same blocks (big geometry only)
   int occ = -1;  // resident CTAs per SM for `search` (lazy, per process)
 };
 
 #define QB_KS(B1, B2, SB, L)                                                                             \
   KernelSet {                                                                                            \
     B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB, false>, table_kernel<B1, B2, SB, L, TPB, true>,     \
-        table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>                          \
+        table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>, nullptr                 \
+  }
+#define QB_KSF(B1, B2, L)                                                                                \
+  KernelSet {                                                                                            \
+    B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB, false>, table_kernel<B1, B2, 0, L, TPB, true>,         \
+        table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>,                           \
+        fieldwalk_kernel<L, TPB>                                                                         \
   }
 
 // Small problems (free bits < BIG_BE): one block of 2^L states per chunk, no sub-blocks.
@@ -79,12 +87,17 @@ static KernelSet g_sets[] = {
 #if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB != 10
     QB_KS(BIG_B1, BIG_B2, BIG_SB, BIG_BE),
 #endif
+#if QB_BIG_SB == 0 && QB_BIG_B1 + QB_BIG_B2 == 10
+    QB_KSF(5, 5, 11), QB_KSF(5, 5, 12), QB_KSF(5, 5, 13), QB_KSF(5, 5, 14), QB_KSF(5, 5, 16), QB_KSF(5, 5, 18),
+    QB_KSF(5, 5, 20), QB_KSF(5, 5, 22),
+#else
 #if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB < 11
     QB_KS(BIG_B1, BIG_B2, BIG_SB, 11),
 #endif
     QB_KS(BIG_B1, BIG_B2, BIG_SB, 12), QB_KS(BIG_B1, BIG_B2, BIG_SB, 13),
     QB_KS(BIG_B1, BIG_B2, BIG_SB, 14), QB_KS(BIG_B1, BIG_B2, BIG_SB, 16),
     QB_KS(BIG_B1, BIG_B2, BIG_SB, 18), QB_KS(BIG_B1, BIG_B2, BIG_SB, 20), QB_KS(BIG_B1, BIG_B2, BIG_SB, 22),
+#endif
 };
 
 static KernelSet* find_set(int BE, int L) {
@@ -305,8 +318,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant != QB_VARIANT_AUTO && variant != QB_VARIANT_TABLE)
-    return fail(QB_E_ARG, "variant not available in this build");
+  if (variant != QB_VARIANT_AUTO && variant != QB_VARIANT_TABLE && variant != QB_VARIANT_FIELDWALK)
+    return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -324,7 +337,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   pl.ks = find_set(BE, L);
   if (!pl.ks) return fail(QB_E_INTERNAL, "no kernel instantiated for BE=" + std::to_string(BE) + " L=" + std::to_string(L));
   pl.B = pl.ks->B1 + pl.ks->B2;
-  if (int rc = quantize(coeffs, n, BE, pl.B, pl)) return rc;
+  // the field walk forms running values over all L free bits in fp32: bound every free bit
+  const bool fieldwalk = variant == QB_VARIANT_FIELDWALK && pl.ks->fieldwalk != nullptr;
+  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl)) return rc;
 
   TableParams& P = *pl.P;
   P.n = n;
@@ -341,7 +356,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   P.chunk_end = ce;
 
   std::memset(out, 0, sizeof(*out));
-  out->variant = QB_VARIANT_TABLE;
+  out->variant = fieldwalk ? QB_VARIANT_FIELDWALK : QB_VARIANT_TABLE;
   out->scale_exp = pl.e;
   out->prefix_bits = pl.k;
   out->exact = pl.exact ? 1 : 0;
@@ -356,12 +371,11 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
 
   KernelSet& ks = *pl.ks;
-  if (ks.occ < 0) {
-    int occ = 0;
-    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.search, TPB, 0));
-    ks.occ = std::max(occ, 1);
-  }
-  const unsigned long long resident = (unsigned long long)ks.occ * dev->sms;
+  const KFn search_fn = fieldwalk ? ks.fieldwalk : ks.search;
+  int occ = 0;
+  QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_fn, TPB, 0));
+  occ = std::max(occ, 1);
+  const unsigned long long resident = (unsigned long long)occ * dev->sms;
   const unsigned long long need_ctas = (nchunks + TPB - 1) / TPB;
   const int grid = (int)std::min(need_ctas, resident);
   if (int rc = ensure(&dev->d_cta, &dev->cta_cap, (size_t)grid)) return rc;
@@ -384,7 +398,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   cudaStream_t st = dev->stream;
   QB_CUDA(cudaMemsetAsync(dev->d_work, 0, sizeof(unsigned long long), st));
   QB_CUDA(cudaEventRecord(dev->ev0, st));
-  ks.search<<<grid, TPB, 0, st>>>(P);
+  search_fn<<<grid, TPB, 0, st>>>(P);
   QB_CUDA(cudaGetLastError());
   QB_CUDA(cudaEventRecord(dev->evs, st));
   ks.finalize<<<1, 1024, 0, st>>>(P);

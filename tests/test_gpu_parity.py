@@ -244,3 +244,33 @@ def test_batch_folds_lower_triangle_like_quboinstance():
     bad[5, 4, 2] = np.inf
     with pytest.raises(ValueError):
         qb.solve_batch(bad)
+
+
+def test_fieldwalk_variant_matches_table_and_golden(golden):
+    """The literal per-step field-walk kernel returns exactly what the table kernel returns."""
+    for case in golden["cases"]:
+        if case["n"] < 12:
+            continue
+        c = np.array(case["coeffs"])
+        for key, want in case["results"].items():
+            if key == "incremental":
+                r = _lib.solve(c, variant=_lib.VARIANT_FIELDWALK)
+                # chunks with more than 10 free bits use the field walk; smaller ones the table kernel
+                assert r.variant == (_lib.VARIANT_FIELDWALK if case["n"] - r.prefix_bits > 10 else _lib.VARIANT_TABLE)
+                assert (r.argmin_bits, r.value) == (want["bits"], want["value"]), case["name"]
+            elif key.startswith("parallel_m"):
+                m = int(key[len("parallel_m"):])
+                r = _lib.solve(c, 0, 0, m, variant=_lib.VARIANT_FIELDWALK)
+                assert (r.argmin_bits, r.value) == (want["bits"], want["value"]), (case["name"], key)
+    for n in (14, 20, 26, 32):
+        for name in ("D", "E"):
+            c = instances.config_coeffs(name, 5, n=n)
+            a = _lib.solve(c)
+            b = _lib.solve(c, variant=_lib.VARIANT_FIELDWALK)
+            assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (name, n)
+            if n == 32:  # 2^21 chunks of 2^11 states: the field walk runs
+                assert b.variant == _lib.VARIANT_FIELDWALK
+    c = _tie_heavy(16, 4242)
+    a = _lib.solve(c, 0, 0, 5)
+    b = _lib.solve(c, 0, 0, 5, variant=_lib.VARIANT_FIELDWALK)
+    assert (a.argmin_bits, a.tie_key) == (b.argmin_bits, b.tie_key)
