@@ -53,20 +53,23 @@ using PFn = void (*)(const TableParams, double*, double*, int);
 
 struct KernelSet {
   int B1, B2, SB, L;
-  KFn search, collect, finalize;
+  KFn search, mark, blocks, states, finalize;
   PFn prefix;
   KFn fieldwalk;  // per-step field-walk search kernel with the same blocks (big geometry only)
+  int occ_fw = -1;  // resident CTAs per SM for `fieldwalk` (lazy)
   int occ = -1;  // resident CTAs per SM for `search` (lazy, per process)
 };
 
 #define QB_KS(B1, B2, SB, L)                                                                             \
   KernelSet {                                                                                            \
-    B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB, false>, table_kernel<B1, B2, SB, L, TPB, true>,     \
+    B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB>, collect_mark_kernel<B1, B2, SB, L>,                \
+        collect_blocks_kernel<B1, B2, SB, L>, collect_states_kernel<B1, B2, SB, L>,                      \
         table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>, nullptr                 \
   }
 #define QB_KSF(B1, B2, L)                                                                                \
   KernelSet {                                                                                            \
-    B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB, false>, table_kernel<B1, B2, 0, L, TPB, true>,         \
+    B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
+        collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
         table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>,                           \
         fieldwalk_kernel<L, TPB>                                                                         \
   }
@@ -119,10 +122,12 @@ struct Device {
   long long* d_chunk_min = nullptr;
   size_t chunk_min_cap = 0;
   unsigned long long* d_cand = nullptr;
-  unsigned long long* d_cand_count = nullptr;
-  unsigned long long* h_cand_count = nullptr;  // pinned
   size_t cand_cap = 0;
   unsigned long long* d_work = nullptr;
+  unsigned long long* d_counts = nullptr;  // [0] chunks, [1] blocks, [2] candidates
+  unsigned long long* h_counts = nullptr;  // pinned
+  unsigned long long* d_lists = nullptr;   // chunk list | block list
+  size_t list_cap = 0;
   double* d_batch_coeffs = nullptr;
   size_t batch_coeffs_cap = 0;
   BatchOut* d_batch_out = nullptr;
@@ -149,9 +154,9 @@ static int get_device(Device** out) {
     QB_CUDA(cudaEventCreate(&d->evs));
     QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
     QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
-    QB_CUDA(cudaMalloc(&d->d_cand_count, sizeof(unsigned long long)));
     QB_CUDA(cudaMalloc(&d->d_work, sizeof(unsigned long long)));
-    QB_CUDA(cudaMallocHost(&d->h_cand_count, sizeof(unsigned long long)));
+    QB_CUDA(cudaMalloc(&d->d_counts, 3 * sizeof(unsigned long long)));
+    QB_CUDA(cudaMallocHost(&d->h_counts, 3 * sizeof(unsigned long long)));
     g_devs[dev] = std::move(d);
   }
   *out = g_devs[dev].get();
@@ -242,16 +247,18 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     P.d[i] = (float)q[(size_t)i * n + i];
     for (int j = i + 1; j < n; ++j) P.Qs[i][j] = P.Qs[j][i] = (float)q[(size_t)i * n + j];
   }
-  for (int z = 0; z < (1 << BMAX); ++z) P.T[z] = 0.f;
-  for (int z = 0; z < (1 << B); ++z) {
-    double t = 0.0;
-    for (int i = 0; i < B; ++i) {
-      if (!((z >> i) & 1)) continue;
-      for (int j = i; j < B; ++j)
-        if ((z >> j) & 1) t += q[(size_t)i * n + j];
+  // T by doubling: T[z + 2^b] = T[z] + q_bb + sum_{i<b} z_i q_ib  (exact integers, |T| < 2^24)
+  P.T[0] = 0.f;
+  for (int b = 0; b < B; ++b) {
+    const double qbb = q[(size_t)b * n + b];
+    for (int z = 0; z < (1 << b); ++z) {
+      double t = (double)P.T[z] + qbb;
+      for (int i = 0; i < b; ++i)
+        if ((z >> i) & 1) t += q[(size_t)i * n + b];
+      P.T[z + (1 << b)] = (float)t;
     }
-    P.T[z] = (float)t;
   }
+  for (int z = (1 << B); z < (1 << BMAX); ++z) P.T[z] = 0.f;
   return QB_OK;
 }
 
@@ -372,9 +379,12 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   KernelSet& ks = *pl.ks;
   const KFn search_fn = fieldwalk ? ks.fieldwalk : ks.search;
-  int occ = 0;
-  QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_fn, TPB, 0));
-  occ = std::max(occ, 1);
+  int& occ = fieldwalk ? ks.occ_fw : ks.occ;
+  if (occ < 0) {
+    int o = 0;
+    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, search_fn, TPB, 0));
+    occ = std::max(o, 1);
+  }
   const unsigned long long resident = (unsigned long long)occ * dev->sms;
   const unsigned long long need_ctas = (nchunks + TPB - 1) / TPB;
   const int grid = (int)std::min(need_ctas, resident);
@@ -390,9 +400,14 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     if (int rc = ensure(&dev->d_chunk_min, &dev->chunk_min_cap, (size_t)nchunks)) return rc;
     P.chunk_min = dev->d_chunk_min;
     if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)1 << 20)) return rc;
+    if (int rc = ensure(&dev->d_lists, &dev->list_cap, (size_t)2 << 20)) return rc;
     P.cand = dev->d_cand;
     P.cand_cap = dev->cand_cap;
-    P.cand_count = dev->d_cand_count;
+    P.cand_count = dev->d_counts + 2;
+    P.counts = dev->d_counts;
+    P.list_cap = dev->list_cap / 2;
+    P.chunk_list = dev->d_lists;
+    P.block_list = dev->d_lists + P.list_cap;
   }
 
   cudaStream_t st = dev->stream;
@@ -427,33 +442,40 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     // certified filter: every state within 2*Eq of the quantized minimum is re-evaluated exactly
     P.mode = MODE_COLLECT;
     P.theta = fo.val + 2 * pl.Eq;
-    QB_CUDA(cudaMemsetAsync(dev->d_cand_count, 0, sizeof(unsigned long long), st));
+    const int grid_mark = std::max(1, std::min((int)((nchunks + 255) / 256), dev->sms * 8));
+    auto run_collect = [&]() -> int {
+      QB_CUDA(cudaMemsetAsync(dev->d_counts, 0, 3 * sizeof(unsigned long long), st));
+      ks.mark<<<grid_mark, 256, 0, st>>>(P);
+      QB_CUDA(cudaGetLastError());
+      ks.blocks<<<dev->sms * 4, 128, 0, st>>>(P);
+      QB_CUDA(cudaGetLastError());
+      ks.states<<<dev->sms * 2, 128, 0, st>>>(P);
+      QB_CUDA(cudaGetLastError());
+      out->launches += 3;
+      QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              st));
+      QB_CUDA(cudaStreamSynchronize(st));
+      return QB_OK;
+    };
     QB_CUDA(cudaEventRecord(dev->ev0, st));
-    ks.collect<<<grid, TPB, 0, st>>>(P);
-    QB_CUDA(cudaGetLastError());
+    if (int rc = run_collect()) return rc;
     QB_CUDA(cudaEventRecord(dev->ev1, st));
-    QB_CUDA(cudaMemcpyAsync(dev->h_cand_count, dev->d_cand_count, sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, st));
-    QB_CUDA(cudaStreamSynchronize(st));
+    QB_CUDA(cudaEventSynchronize(dev->ev1));
     QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
     out->kernel_ms += ms;
     out->collect_ms = ms;
-    out->launches += 1;
-    unsigned long long cnt = *dev->h_cand_count;
+    if (dev->h_counts[0] > P.list_cap || dev->h_counts[1] > P.list_cap)
+      return fail(QB_E_INTERNAL, "collect pass: more than " + std::to_string(P.list_cap) +
+                                     " chunks or blocks within the certified bound");
+    unsigned long long cnt = dev->h_counts[2];
     if (cnt == 0) return fail(QB_E_INTERNAL, "collect pass found no candidate");
     if (cnt > P.cand_cap && all_out != nullptr && cnt <= (1ull << 27)) {
       // all-minimisers request with more ties than the buffer holds: grow it and collect again
       if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)cnt)) return rc;
       P.cand = dev->d_cand;
       P.cand_cap = dev->cand_cap;
-      QB_CUDA(cudaMemsetAsync(dev->d_cand_count, 0, sizeof(unsigned long long), st));
-      ks.collect<<<grid, TPB, 0, st>>>(P);
-      QB_CUDA(cudaGetLastError());
-      out->launches += 1;
-      QB_CUDA(cudaMemcpyAsync(dev->h_cand_count, dev->d_cand_count, sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost, st));
-      QB_CUDA(cudaStreamSynchronize(st));
-      cnt = *dev->h_cand_count;
+      if (int rc = run_collect()) return rc;
+      cnt = dev->h_counts[2];
     }
     if (cnt > P.cand_cap)
       return fail(QB_E_INTERNAL, "more than " + std::to_string(P.cand_cap) + " near-tied minimisers (float path)");
@@ -640,11 +662,12 @@ void qb_shutdown(void) {
     cudaFreeHost(d->h_final);
     cudaFree(d->d_chunk_min);
     cudaFree(d->d_cand);
-    cudaFree(d->d_cand_count);
     cudaFree(d->d_work);
+    cudaFree(d->d_counts);
+    cudaFreeHost(d->h_counts);
+    cudaFree(d->d_lists);
     cudaFree(d->d_batch_coeffs);
     cudaFree(d->d_batch_out);
-    cudaFreeHost(d->h_cand_count);
     cudaEventDestroy(d->ev0);
     cudaEventDestroy(d->ev1);
     cudaEventDestroy(d->evs);

@@ -55,6 +55,10 @@ struct alignas(16) TableParams {
   Rec* cta_out;                    // one record per CTA
   FinalOut* final_out;
   unsigned long long* work;        // dynamic chunk counter (zeroed before each search launch)
+  unsigned long long* counts;      // collect pass counters: [0] chunks, [1] blocks, [2] unused
+  unsigned long long* chunk_list;  // chunk offsets (c - chunk_begin) whose minimum is <= theta
+  unsigned long long* block_list;  // (chunk offset << 32) | block j, block minimum <= theta
+  unsigned long long list_cap;
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };

@@ -84,8 +84,20 @@ __host__ __device__ constexpr int ctz_c(int k) { return (k & 1) ? 0 : 1 + ctz_c(
 // Gray order, delta_s = the sub-block bits' own value given the outer state (uses F).
 // Per state: half an FADD2 (two states, T pair from the constant bank through uniform
 // registers), half an FMNMX3, and 1/(2P) of an LDCU.128.
+#ifndef QB_TSMEM
+#define QB_TSMEM 0  // 1: stage T in shared memory and read it with broadcast LDS.128
+#endif
+
+
+__device__ __forceinline__ float4 t_lds128(unsigned addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 template <int B1, int B2, int SB, int NF>
-__device__ __forceinline__ float block_min_p1(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
+__device__ __forceinline__ float block_min_p1(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF],
+                                              unsigned tsm = 0) {
   constexpr int B = B1 + B2, NU = 1 << B1, NW = 1 << B2, P = 1 << SB;
   static_assert(B2 >= 1, "inner low part needs at least one bit");
   float rmin = 0.f;
@@ -123,21 +135,33 @@ __device__ __forceinline__ float block_min_p1(const TableParams& p, const float 
 #pragma unroll
       for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + hs[B2 + i];
 #pragma unroll
-    for (int u = 0; u < NU; u += 2) {
+    for (int kk = 0; kk < NU; kk += 2) {
       float ru[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (u + h >= NU) { ru[h] = ru[0]; continue; }
+        if (kk + h >= NU) { ru[h] = ru[0]; continue; }
+        const int u = kk + h;
         float acc = 0.f;
+        if constexpr (QB_TSMEM && NW >= 4) {
 #pragma unroll
-        for (int w = 0; w < NW; w += 2) {
-          const float2 t = *reinterpret_cast<const float2*>(&p.T[(u + h) * NW + w]);
-          const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
-          acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
+          for (int w = 0; w < NW; w += 4) {
+            const float4 t4 = t_lds128(tsm + 4u * (u * NW + w));
+            const float2 c0 = add_f32x2(make_float2(Bw[w], Bw[w + 1]), make_float2(t4.x, t4.y));
+            const float2 c1 = add_f32x2(make_float2(Bw[w + 2], Bw[w + 3]), make_float2(t4.z, t4.w));
+            acc = (w == 0) ? fminf(c0.x, c0.y) : fminf(fminf(acc, c0.x), c0.y);
+            acc = fminf(fminf(acc, c1.x), c1.y);
+          }
+        } else {
+#pragma unroll
+          for (int w = 0; w < NW; w += 2) {
+            const float2 t = *reinterpret_cast<const float2*>(&p.T[u * NW + w]);
+            const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
+            acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
+          }
         }
-        ru[h] = acc + A[u + h];
+        ru[h] = acc + A[u];
       }
-      rmin = (s == 0 && u == 0) ? fminf(ru[0], ru[1]) : fminf(fminf(rmin, ru[0]), ru[1]);
+      rmin = (s == 0 && kk == 0) ? fminf(ru[0], ru[1]) : fminf(fminf(rmin, ru[0]), ru[1]);
     }
   }
   return rmin;
@@ -215,8 +239,9 @@ __device__ __forceinline__ float block_min_shared(const TableParams& p, const fl
 }
 
 template <int B1, int B2, int SB, int NF>
-__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
-  if constexpr (SB == 0) return block_min_p1<B1, B2, SB, NF>(p, H, F);
+__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF],
+                                           unsigned tsm = 0) {
+  if constexpr (SB == 0) return block_min_p1<B1, B2, SB, NF>(p, H, F, tsm);
   else return block_min_shared<B1, B2, SB, NF>(p, H, F);
 }
 
@@ -242,49 +267,93 @@ __device__ __forceinline__ void for_block_states(const TableParams& p, unsigned 
   }
 }
 
-template <int B, int SB, int L>
-__device__ __noinline__ void collect_block(const TableParams& p, unsigned long long s, unsigned int j) {
-  constexpr int BE = B + SB;
-  const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
-  for_block_states<B, SB, L>(p, xo, 0, 1, [&](unsigned int zb, long long val) {
-    if (val <= p.theta) {
-      const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
-      if (idx < p.cand_cap) p.cand[idx] = xo | zb;
+// ---- certified-filter collect pass (float path / all-minimisers), three small launches:
+// 1. chunks whose recorded minimum is <= theta -> chunk_list
+template <int B1, int B2, int SB, int L>
+__global__ void __launch_bounds__(256) collect_mark_kernel(const __grid_constant__ TableParams p) {
+  const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+  for (unsigned long long ci = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; ci < nchunks;
+       ci += (unsigned long long)gridDim.x * blockDim.x) {
+    if (p.chunk_min[ci] <= p.theta) {
+      const unsigned long long idx = atomicAdd(&p.counts[0], 1ull);
+      if (idx < p.list_cap) p.chunk_list[idx] = ci;
     }
-  });
+  }
 }
 
-template <int B1, int B2, int SB, int L, int TPB, bool COLLECT>
+// 2. one thread per (listed chunk, block): block base by direct evaluation, table block minimum,
+//    blocks <= theta -> block_list
+template <int B1, int B2, int SB, int L>
+__global__ void __launch_bounds__(128) collect_blocks_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2, BE = B + SB, LO = L - BE;
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  const unsigned long long nlisted = min(p.counts[0], p.list_cap);
+  const unsigned long long total = nlisted << LO;
+  for (unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long ci = p.chunk_list[g >> LO];
+    const unsigned int j = (unsigned int)(g & ((1ull << LO) - 1ull));
+    const unsigned long long s = chunk_prefix(p, p.chunk_begin + ci);
+    const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
+    long long V;
+    float H[B], F[NF];
+    base_eval<B, L>(p, xo, B, V, H, F);
+    if (V + (long long)block_min<B1, B2, SB, NF>(p, H, F) <= p.theta) {
+      const unsigned long long idx = atomicAdd(&p.counts[1], 1ull);
+      if (idx < p.list_cap) p.block_list[idx] = (ci << 32) | j;
+    }
+  }
+}
+
+// 3. one warp per listed block: every state <= theta -> cand
+template <int B1, int B2, int SB, int L>
+__global__ void __launch_bounds__(128) collect_states_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2, BE = B + SB;
+  const unsigned long long nblocks = min(p.counts[1], p.list_cap);
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long w = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nblocks;
+       w += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+    const unsigned long long e = p.block_list[w];
+    const unsigned long long ci = e >> 32;
+    const unsigned int j = (unsigned int)(e & 0xffffffffu);
+    const unsigned long long s = chunk_prefix(p, p.chunk_begin + ci);
+    const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
+    for_block_states<B, SB, L>(p, xo, lane, 32, [&](unsigned int zb, long long val) {
+      if (val <= p.theta) {
+        const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
+        if (idx < p.cand_cap) p.cand[idx] = xo | zb;
+      }
+    });
+  }
+}
+
+template <int B1, int B2, int SB, int L, int TPB>
 __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   constexpr int BE = B + SB;
   constexpr int LO = L - BE;
   constexpr int NF = (L - B) > 0 ? (L - B) : 1;
   static_assert(LO >= 0, "block bits exceed chunk bits");
+  unsigned tsm_base = 0;
+  if constexpr (QB_TSMEM) {
+    __shared__ __align__(16) float sT[1 << B];
+    for (int z = threadIdx.x; z < (1 << B); z += TPB) sT[z] = p.T[z];
+    __syncthreads();
+    tsm_base = (unsigned)__cvta_generic_to_shared(sT);
+  }
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
   const int lane = threadIdx.x & 31;
-  // Work distribution: the search pass hands out 32 consecutive chunks per warp from a global
-  // counter (one atomic per 32 chunks) so all SMs finish within one chunk of each other; the
-  // collect pass (few chunks survive its filter) is a plain grid-stride loop.
-  unsigned long long next = (unsigned long long)blockIdx.x * TPB + threadIdx.x;
-  const unsigned long long stride = (unsigned long long)gridDim.x * TPB;
+  // Work distribution: 32 consecutive chunks per warp from a global counter (one atomic per 32
+  // chunks), so all SMs finish within one chunk of each other.
   for (;;) {
-    unsigned long long ci;
-    if (COLLECT) {
-      ci = next;
-      next += stride;
-      if (ci >= nchunks) break;
-    } else {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(p.work, 32ull);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base >= nchunks) break;
-      ci = base + lane;
-      if (ci >= nchunks) continue;
-    }
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(p.work, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= nchunks) break;
+    const unsigned long long ci = base + lane;
+    if (ci >= nchunks) continue;
     const unsigned long long c = p.chunk_begin + ci;
-    if (COLLECT && p.chunk_min[ci] > p.theta) continue;
     const unsigned long long s = chunk_prefix(p, c);
     long long V;
     float H[B], F[NF];
@@ -298,21 +367,18 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
         const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
         outer_flip<B, L, BE>(p, BE + r, sg, V, H, F);
       }
-      const float rm = block_min<B1, B2, SB, NF>(p, H, F);
+      unsigned tsm = tsm_base;
+      if constexpr (QB_TSMEM) asm volatile("" : "+r"(tsm));  // no hoisting of table loads across blocks
+      const float rm = block_min<B1, B2, SB, NF>(p, H, F, tsm);
       const long long val = V + (long long)rm;
-      if (COLLECT) {
-        if (val <= p.theta) collect_block<B, SB, L>(p, s, j);
-        continue;
-      }
       cmin = min(cmin, val);
       if (val <= best.val) {
         const unsigned long long K = block_key(p, key_hi, dir, j, LO);
         if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
       }
     }
-    if (!COLLECT && p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
+    if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
-  if (COLLECT) return;
   const Rec r = cta_reduce<TPB>(best);
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
 }
