@@ -45,7 +45,7 @@ CONFIG_DESC = {
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
 # SASS instructions per state of the table kernel's inner block (cuobjdump count)
-SASS_INSTR_PER_STATE = 1.52  # ncu smsp__inst_executed x 32 / 2^40 (profiles/r01_ncu_search_summary.txt)
+SASS_INSTR_PER_STATE = 1.48  # ncu smsp__inst_executed x 32 / 2^40 (profiles/r02_ncu_search_summary.txt)
 
 
 def parse():
