@@ -41,7 +41,9 @@ CONFIG_DESC = {
     "D": "D: n=32 int32 U[-1000,1000], single instance",
     "E": "E: n=40 fp32 N(0,1), 10% off-diagonal density, dense diagonal",
 }
-# measured FP32 add-lane issue peak per SM per clock (tools/alu_peaks.cu, profiles/r01_alu_peaks.json)
+# FP32 add-lane peak: measured on this pool's B200 by tools/alu_peaks.cu (profiles/r01_alu_peaks.json,
+# CUDA events, 2 CTAs x 512 threads/SM); fallback = 128 lanes/SM/clk x SMs x max SM clock
+ALU_PEAKS = os.path.join(ROOT, "profiles", "r01_alu_peaks.json")
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
 # SASS instructions per state of the table kernel's inner block (cuobjdump count)
@@ -315,13 +317,20 @@ def main():
     search_s = search_ms_max * 1e-3 / args.steps
     achieved = per_launch_states * (n + 1) / search_s
     peak = FP32_ADD_LANES_PER_SM_CLK * sm_count * sm_hz
+    peak_src = "fallback 128 lanes/SM/clk x SMs x max SM clock"
+    try:
+        with open(ALU_PEAKS) as fh:
+            peak = float(json.load(fh)["results"]["fadd2"]["lane_ops_per_s"])
+        peak_src = "measured FP32 add-lane rate (tools/alu_peaks.cu, profiles/r01_alu_peaks.json)"
+    except (OSError, KeyError, ValueError):
+        pass
     issue_peak = ISSUE_WARP_INSTR_PER_SM_CLK * 32 * sm_count * sm_hz
     roofline = {
         "bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
         "frac": achieved / peak, "traffic": None,
-        "basis": f"nominal {n + 1} ops/state (SURVEY.md §8d: n-1 field adds + 1 value add + 1 min) vs the measured "
-                 "FP32 add-lane peak (128 lanes/SM/clk x SMs x max SM clock); the table kernel issues "
-                 f"~{SASS_INSTR_PER_STATE} SASS instr/state, so frac > 1 measures the algorithmic saving",
+        "basis": f"nominal {n + 1} ops/state (SURVEY.md §8d: n-1 field adds + 1 value add + 1 min) vs the "
+                 f"{peak_src}; the table kernel issues ~{SASS_INSTR_PER_STATE} SASS instr/state, so frac > 1 "
+                 "measures the algorithmic saving and issue_frac (vs 4 warp-instr/SM/clk) the kernel quality",
         "issue_frac": per_launch_states * SASS_INSTR_PER_STATE / search_s / issue_peak,
         "search_ms_per_launch": search_s * 1e3,
     }
