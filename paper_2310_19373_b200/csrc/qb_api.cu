@@ -270,10 +270,15 @@ static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int
     return QB_OK;
   }
   BE = BIG_BE;
-  // ~16 chunks per resident thread on every shard (dynamic scheduling keeps the tail to one chunk)
-  const double want_chunks = 16.0 * sms * QB_MINB * TPB * (double)shard_count;
+  // ~4 chunks per resident thread on every shard: large chunks amortise the chunk-start evaluation,
+  // dynamic scheduling keeps the tail to one chunk (measured optimum on B200: n=40 -> k=20, n=32 -> k=18)
+#ifndef QB_CHUNKS_PER_THREAD
+#define QB_CHUNKS_PER_THREAD 4
+#endif
+  const double want_chunks = (double)QB_CHUNKS_PER_THREAD * sms * QB_MINB * TPB * (double)shard_count;
   int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
   int Lw = n - want_k;
+  if (Lw & 1) Lw += (Lw < 16) ? 1 : -1;  // even chunk sizes: round up for small, down for large chunks
   Lw = std::max(Lw, BIG_BE);
   Lw = std::min(Lw, std::min(22, lmax));
   if (Lw > 14) Lw = 2 * (Lw / 2);

@@ -22,6 +22,9 @@
 #pragma once
 #include "qb_common.cuh"
 
+#ifndef QB_PREFIX_UNROLL
+#define QB_PREFIX_UNROLL 1  // unroll of the chunk-start evaluation loop over prefix bits
+#endif
 #ifndef QB_MINB
 #define QB_MINB 5  // resident CTAs per SM requested from ptxas: caps registers at 96 (20 warps/SM)
 #endif
@@ -43,6 +46,8 @@ __device__ __forceinline__ void base_eval(const TableParams& p, unsigned long lo
 #pragma unroll
   for (int m = 0; m < ((L - B) > 0 ? (L - B) : 1); ++m) F[m] = 0.f;
   V = 0;
+  constexpr int kUnroll = QB_PREFIX_UNROLL;
+#pragma unroll kUnroll
   for (int q = q_start; q < p.n; ++q) {
     const float xq = ((x >> q) & 1ull) ? 1.f : 0.f;
 #pragma unroll
