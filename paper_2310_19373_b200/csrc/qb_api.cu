@@ -128,6 +128,10 @@ struct Device {
   unsigned long long* h_counts = nullptr;  // pinned
   unsigned long long* d_lists = nullptr;   // chunk list | block list
   size_t list_cap = 0;
+  double* d_coeffs = nullptr;              // fp64 coefficients for the overflow reduction
+  size_t coeffs_cap = 0;
+  unsigned long long* d_red = nullptr;     // [0] value key, [1] tie key
+  unsigned long long* h_red = nullptr;     // pinned
   double* d_batch_coeffs = nullptr;
   size_t batch_coeffs_cap = 0;
   BatchOut* d_batch_out = nullptr;
@@ -157,6 +161,8 @@ static int get_device(Device** out) {
     QB_CUDA(cudaMalloc(&d->d_work, sizeof(unsigned long long)));
     QB_CUDA(cudaMalloc(&d->d_counts, 3 * sizeof(unsigned long long)));
     QB_CUDA(cudaMallocHost(&d->h_counts, 3 * sizeof(unsigned long long)));
+    QB_CUDA(cudaMalloc(&d->d_red, 2 * sizeof(unsigned long long)));
+    QB_CUDA(cudaMallocHost(&d->h_red, 2 * sizeof(unsigned long long)));
     g_devs[dev] = std::move(d);
   }
   *out = g_devs[dev].get();
@@ -291,6 +297,14 @@ static unsigned long long host_tie_key(unsigned long long x, int n, int m_tie, i
   const int lo = n - m_tie;
   const unsigned long long lowmask = mask64(lo);
   return (x & ~lowmask) | ginv64(x & lowmask);
+}
+
+static unsigned long long host_key_to_state(unsigned long long key, int n, int m_tie, int rule) {
+  if (rule == RULE_INTEGER) return key;
+  const int lo = n - m_tie;
+  const unsigned long long lowmask = mask64(lo);
+  const unsigned long long t = key & lowmask;
+  return (key & ~lowmask) | (t ^ (t >> 1));
 }
 
 static unsigned long long ordered_double(double v) {
@@ -482,8 +496,40 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
       if (int rc = run_collect()) return rc;
       cnt = dev->h_counts[2];
     }
-    if (cnt > P.cand_cap)
-      return fail(QB_E_INTERNAL, "more than " + std::to_string(P.cand_cap) + " near-tied minimisers (float path)");
+    if (cnt > P.cand_cap) {
+      if (all_out != nullptr)
+        return fail(QB_E_INTERNAL, "more than " + std::to_string(P.cand_cap) + " minimisers requested");
+      // more near-ties than the candidate buffer: reduce them on the device instead -- exact fp64
+      // value of every candidate (reference eval_upper order), then the lowest tie key among the
+      // candidates attaining the minimum value
+      if (int rc = ensure(&dev->d_coeffs, &dev->coeffs_cap, (size_t)n * n)) return rc;
+      QB_CUDA(cudaMemcpyAsync(dev->d_coeffs, coeffs, (size_t)n * n * sizeof(double), cudaMemcpyHostToDevice, st));
+      P.coeffs64 = dev->d_coeffs;
+      P.red = dev->d_red;
+      QB_CUDA(cudaMemsetAsync(dev->d_red, 0xff, 2 * sizeof(unsigned long long), st));
+      const int nstates_grid = dev->sms * 2;
+      P.mode = MODE_REDUCE_VALUE;
+      ks.states<<<nstates_grid, 128, 0, st>>>(P);
+      QB_CUDA(cudaGetLastError());
+      P.mode = MODE_REDUCE_KEY;
+      ks.states<<<nstates_grid, 128, 0, st>>>(P);
+      QB_CUDA(cudaGetLastError());
+      out->launches += 2;
+      QB_CUDA(cudaMemcpyAsync(dev->h_red, dev->d_red, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      QB_CUDA(cudaStreamSynchronize(st));
+      const unsigned long long key = dev->h_red[1];
+      if (key == ~0ull) return fail(QB_E_INTERNAL, "overflow reduction found no candidate");
+      const unsigned long long x = host_key_to_state(key, n, m_tie, rule);
+      out->candidates = cnt;
+      out->argmin_bits = x;
+      out->tie_key = key;
+      out->value = eval_bits(coeffs, n, x);
+      out->value_key = ordered_double(out->value);
+      if (out->value_key != dev->h_red[0]) return fail(QB_E_INTERNAL, "device and host eval_upper disagree");
+      out->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+      return QB_OK;
+    }
     std::vector<unsigned long long> cand(cnt);
     QB_CUDA(cudaMemcpyAsync(cand.data(), dev->d_cand, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     QB_CUDA(cudaStreamSynchronize(st));
@@ -671,6 +717,9 @@ void qb_shutdown(void) {
     cudaFree(d->d_counts);
     cudaFreeHost(d->h_counts);
     cudaFree(d->d_lists);
+    cudaFree(d->d_coeffs);
+    cudaFree(d->d_red);
+    cudaFreeHost(d->h_red);
     cudaFree(d->d_batch_coeffs);
     cudaFree(d->d_batch_out);
     cudaEventDestroy(d->ev0);

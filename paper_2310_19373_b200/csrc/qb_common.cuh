@@ -59,10 +59,14 @@ struct alignas(16) TableParams {
   unsigned long long* chunk_list;  // chunk offsets (c - chunk_begin) whose minimum is <= theta
   unsigned long long* block_list;  // (chunk offset << 32) | block j, block minimum <= theta
   unsigned long long list_cap;
+  const double* coeffs64;          // original fp64 coefficients (device), for the overflow reduction
+  unsigned long long* red;         // [0] best ordered value, [1] best tie key (overflow reduction)
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };
-enum { MODE_SEARCH = 0, MODE_SEARCH_RECORD = 1, MODE_COLLECT = 2 };
+enum { MODE_SEARCH = 0, MODE_SEARCH_RECORD = 1, MODE_COLLECT = 2, MODE_REDUCE_VALUE = 3, MODE_REDUCE_KEY = 4 };
+
+
 
 __host__ __device__ __forceinline__ unsigned long long ginv64(unsigned long long x) {
   // inverse reflected Gray code (prefix XOR from the top): step index at which x is visited
@@ -143,6 +147,33 @@ __device__ __forceinline__ Rec cta_reduce(Rec r, int nwarps = TPB / 32) {
     }
   }
   return r;
+}
+
+// eval_upper (_kernels.py:12-20) on the device: same row-major fp64 order, no FMA contraction
+__device__ __forceinline__ double eval_upper_dev(const double* c, int n, unsigned long long x) {
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double xi = (double)((x >> i) & 1ull);
+    for (int j = i; j < n; ++j) {
+      const double xj = (double)((x >> j) & 1ull);
+      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c[i * n + j], xi), xj));
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ unsigned long long ordered_f64(double v) {
+  if (v == 0.0) v = 0.0;  // canonicalise -0.0
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+// tie key of a state, host and device (same formula as qb_api.cu host_tie_key)
+__device__ __forceinline__ unsigned long long state_tie_key(unsigned long long x, int n, int m_tie, int rule) {
+  if (rule == RULE_INTEGER) return x;
+  const int lo = n - m_tie;
+  const unsigned long long lowmask = mask64(lo);
+  return (x & ~lowmask) | ginv64(x & lowmask);
 }
 
 }  // namespace qb

@@ -324,9 +324,16 @@ __global__ void __launch_bounds__(128) collect_states_kernel(const __grid_consta
     const unsigned long long s = chunk_prefix(p, p.chunk_begin + ci);
     const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
     for_block_states<B, SB, L>(p, xo, lane, 32, [&](unsigned int zb, long long val) {
-      if (val <= p.theta) {
+      if (val > p.theta) return;
+      const unsigned long long x = xo | zb;
+      if (p.mode == MODE_COLLECT) {
         const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
-        if (idx < p.cand_cap) p.cand[idx] = xo | zb;
+        if (idx < p.cand_cap) p.cand[idx] = x;
+      } else {
+        // overflow path: exact fp64 value of every candidate, lexicographic (value, key) minimum
+        const unsigned long long vk = ordered_f64(eval_upper_dev(p.coeffs64, p.n, x));
+        if (p.mode == MODE_REDUCE_VALUE) atomicMin(&p.red[0], vk);
+        else if (vk == p.red[0]) atomicMin(&p.red[1], state_tie_key(x, p.n, p.m_tie, p.rule));
       }
     });
   }

@@ -274,3 +274,22 @@ def test_fieldwalk_variant_matches_table_and_golden(golden):
     a = _lib.solve(c, 0, 0, 5)
     b = _lib.solve(c, 0, 0, 5, variant=_lib.VARIANT_FIELDWALK)
     assert (a.argmin_bits, a.tie_key) == (b.argmin_bits, b.tie_key)
+
+
+def test_float_path_massive_ties_device_reduction():
+    """A non-quantizable (fp64) instance with 2^21 exactly tied minimisers: more than the 2^20
+    candidate buffer, so the device re-evaluates every candidate in fp64 and reduces (value, key)."""
+    n = 24
+    c = np.zeros((n, n))
+    rng = np.random.default_rng(5)
+    core = np.triu(rng.uniform(-1, 1, size=(3, 3)))
+    c[21:, 21:] = core  # bits 0..20 are decoupled with zero cost: every minimum is 2^21-fold tied
+    inst = qb.QuboInstance(c)
+    res = _lib.solve(inst.coeffs)
+    assert res.exact == 0 and res.candidates > (1 << 20)
+    bits, val, _ = O.expected_argmin(c, 0)
+    assert int(res.argmin_bits) == bits and res.value == val
+    for m in (3, 22):
+        bits_m, _, _ = O.expected_argmin(c, m)
+        r = _lib.solve(inst.coeffs, 0, 0, m)
+        assert int(r.argmin_bits) == bits_m, m
