@@ -18,6 +18,7 @@
 // instance on the single-instance path.
 #pragma once
 #include "qb_common.cuh"
+#include "qb_table.cuh"
 
 namespace qb {
 
@@ -59,17 +60,9 @@ template <int B1, int B2>
 __device__ __forceinline__ float batch_block_min(unsigned sT, const float (&H)[B1 + B2]) {
   constexpr int NU = 1 << B1, NW = 1 << B2;
   float Bw[NW];
-  Bw[0] = 0.f;
-#pragma unroll
-  for (int i = 0; i < B2; ++i)
-#pragma unroll
-    for (int w = 0; w < (1 << i); ++w) Bw[w + (1 << i)] = Bw[w] + H[i];
+  subset_sums<B2>(Bw, 0.f, H);
   float A[NU];
-  A[0] = 0.f;
-#pragma unroll
-  for (int i = 0; i < B1; ++i)
-#pragma unroll
-    for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + H[B2 + i];
+  subset_sums<B1>(A, 0.f, H + B2);
   float rmin = 0.f;
 #pragma unroll
   for (int u = 0; u < NU; ++u) {

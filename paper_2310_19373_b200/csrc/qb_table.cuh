@@ -81,6 +81,24 @@ __device__ __forceinline__ void outer_flip(const TableParams& p, int ell, float 
 
 __host__ __device__ constexpr int ctz_c(int k) { return (k & 1) ? 0 : 1 + ctz_c(k >> 1); }
 
+// S[m] = base + sum_{i : bit i of m} h[i] for m < 2^NB; S[m + 2^i] = S[m] + h[i], pairs via FADD2
+template <int NB>
+__device__ __forceinline__ void subset_sums(float* S, float base, const float* h) {
+  S[0] = base;
+  if constexpr (NB > 0) {
+    S[1] = base + h[0];
+#pragma unroll
+    for (int i = 1; i < NB; ++i) {
+#pragma unroll
+      for (int m = 0; m < (1 << i); m += 2) {
+        const float2 r = __fadd2_rn(make_float2(S[m], S[m + 1]), make_float2(h[i], h[i]));
+        S[m + (1 << i)] = r.x;
+        S[m + 1 + (1 << i)] = r.y;
+      }
+    }
+  }
+}
+
 // Minimum over the 2^(B+SB) states of a super-block, relative to its base value V (all block
 // bits zero).  The B table bits are split into u (B1 high) and w (B2 low); the SB sub-block
 // bits (positions B..B+SB-1) select one of P = 2^SB sub-blocks that share every table load:
@@ -126,19 +144,12 @@ __device__ __forceinline__ float block_min_p1(const TableParams& p, const float 
       for (int t2 = t + 1; t2 < SB; ++t2)
         if ((s >> t2) & 1) dl += p.Qs[B + t][B + t2];
     }
-    // subset sums: Bw over the w bits, A over the u bits (independent adds, no serial chain)
+    // subset sums: Bw over the w bits, A over the u bits (independent adds, no serial chain);
+    // from the second bit on, pairs of sums are extended with one packed FADD2
     float Bw[NW];
-    Bw[0] = 0.f;
-#pragma unroll
-    for (int i = 0; i < B2; ++i)
-#pragma unroll
-      for (int w = 0; w < (1 << i); ++w) Bw[w + (1 << i)] = Bw[w] + hs[i];
+    subset_sums<B2>(Bw, 0.f, hs);
     float A[NU];
-    A[0] = dl;
-#pragma unroll
-    for (int i = 0; i < B1; ++i)
-#pragma unroll
-      for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + hs[B2 + i];
+    subset_sums<B1>(A, dl, hs + B2);
 #pragma unroll
     for (int kk = 0; kk < NU; kk += 2) {
       float ru[2];
