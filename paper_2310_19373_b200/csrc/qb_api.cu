@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -56,8 +57,8 @@ struct KernelSet {
   KFn search, mark, blocks, states, finalize;
   PFn prefix;
   KFn fieldwalk;  // per-step field-walk search kernel with the same blocks (big geometry only)
-  int occ_fw = -1;  // resident CTAs per SM for `fieldwalk` (lazy)
-  int occ = -1;  // resident CTAs per SM for `search` (lazy, per process)
+  std::atomic<int> occ_fw{-1};  // resident CTAs per SM for `fieldwalk` (lazy)
+  std::atomic<int> occ{-1};  // resident CTAs per SM for `search` (lazy; shared by all devices)
 };
 
 #define QB_KS(B1, B2, SB, L)                                                                             \
@@ -398,11 +399,13 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   KernelSet& ks = *pl.ks;
   const KFn search_fn = fieldwalk ? ks.fieldwalk : ks.search;
-  int& occ = fieldwalk ? ks.occ_fw : ks.occ;
+  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : ks.occ;
+  int occ = occ_cache.load();
   if (occ < 0) {
     int o = 0;
     QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, search_fn, TPB, 0));
     occ = std::max(o, 1);
+    occ_cache.store(occ);
   }
   const unsigned long long resident = (unsigned long long)occ * dev->sms;
   const unsigned long long need_ctas = (nchunks + TPB - 1) / TPB;

@@ -293,3 +293,29 @@ def test_float_path_massive_ties_device_reduction():
         bits_m, _, _ = O.expected_argmin(c, m)
         r = _lib.solve(inst.coeffs, 0, 0, m)
         assert int(r.argmin_bits) == bits_m, m
+
+
+@pytest.mark.parametrize("n,m", [(30, 2), (32, 5), (34, 9), (36, 14)])
+def test_large_geometry_subspaces_vs_oracle(n, m):
+    """Large chunks (outer Gray walk active) with fixed suffix bits: solve_subspace against the
+    CPU oracle's exact scan of the same subspace, integer and float instances."""
+    rng = np.random.default_rng(n * 100 + m)
+    for name in ("D", "E"):
+        c = instances.config_coeffs(name, 7, n=n)
+        inst = qb.QuboInstance(c)
+        for suffix in rng.integers(0, 1 << m, size=2):
+            suffix = int(suffix)
+            bits, val, ev = O.solve_subspaces(c, m, suffix, suffix + 1)
+            sol = qb.solve_subspace(inst, qb.SubspaceSpec(m, suffix))
+            assert (_bits(sol), sol.value, sol.evaluations) == (bits, val, ev), (name, n, m, suffix)
+
+
+def test_large_geometry_parallel_tie_rule_vs_oracle():
+    """solve_parallel(m) at n=30 with many exact ties ({-1,0,1} entries): the (suffix, local Gray
+    rank) rule on the large-chunk geometry against the reference-order oracle."""
+    c = _tie_heavy(30, 777, -1, 1)
+    inst = qb.QuboInstance(c)
+    for m in (0, 3):
+        bits, val, ev = O.solve_subspaces(c, m, threads=16)
+        sol = qb.solve_parallel(inst, qb.SolveConfig(threads=8, fixed_bits=m))
+        assert (_bits(sol), sol.value, sol.evaluations) == (bits, val, ev), m
