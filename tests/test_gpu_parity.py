@@ -319,3 +319,35 @@ def test_large_geometry_parallel_tie_rule_vs_oracle():
         bits, val, ev = O.solve_subspaces(c, m, threads=16)
         sol = qb.solve_parallel(inst, qb.SolveConfig(threads=8, fixed_bits=m))
         assert (_bits(sol), sol.value, sol.evaluations) == (bits, val, ev), m
+
+
+def _adversarial(kind, n, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "big_int":  # |Q| up to 2^30: sums exceed the fp32 exactness bound -> scale-down, filter path
+        c = rng.integers(-(1 << 30), 1 << 30, size=(n, n)).astype(np.float64)
+    elif kind == "wide_range":  # 1e-10 .. 1e10 magnitudes
+        c = rng.standard_normal((n, n)) * 10.0 ** rng.integers(-10, 11, size=(n, n))
+    elif kind == "tiny":  # around 1e-300 incl. subnormals
+        c = rng.standard_normal((n, n)) * 1e-300
+        c[0, 0] = 5e-320
+    elif kind == "neg_zero":
+        c = rng.integers(-2, 3, size=(n, n)).astype(np.float64)
+        c[c == 0] = -0.0
+    elif kind == "dyadic":  # exactly representable after scaling: exact path with e > 0
+        c = rng.integers(-64, 65, size=(n, n)) / 1024.0
+    return np.triu(c)
+
+
+@pytest.mark.parametrize("kind", ["big_int", "wide_range", "tiny", "neg_zero", "dyadic"])
+def test_adversarial_value_ranges_vs_oracle(kind):
+    for n in (9, 14, 22):
+        for seed in range(3):
+            c = _adversarial(kind, n, 1000 * n + seed)
+            inst = qb.QuboInstance(c)
+            bits, val, ev = O.solve_incremental(inst.coeffs)
+            sol = qb.solve_incremental(inst)
+            assert (_bits(sol), sol.value) == (bits, val), (kind, n, seed)
+            m = 3
+            bits, val, _ = O.solve_subspaces(inst.coeffs, m)
+            sol = qb.solve_parallel(inst, qb.SolveConfig(threads=2, fixed_bits=m))
+            assert (_bits(sol), sol.value) == (bits, val), (kind, n, seed, m)
