@@ -42,9 +42,10 @@ extern "C" {
 #define QB_TIE_INTEGER 1   /* lowest integer encoding: solve_naive -- solver.py:99-115, _kernels.py:23-43 */
 
 /* Traversal kernel variants. */
-#define QB_VARIANT_AUTO 0      /* table kernel (fastest exact path) */
-#define QB_VARIANT_TABLE 1     /* blocked Gray walk: outer field updates + inner-block table */
+#define QB_VARIANT_AUTO 0      /* fastest: coarse-filter kernel for large chunks, table kernel otherwise */
+#define QB_VARIANT_TABLE 1     /* blocked Gray walk: outer field updates + inner-block fp32 table */
 #define QB_VARIANT_FIELDWALK 2 /* per-step Gray walk with register local fields (Alg. 1 form) */
+#define QB_VARIANT_COARSE 3    /* table walk with a packed-int16 block pass + exact re-evaluation */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {

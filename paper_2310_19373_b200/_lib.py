@@ -35,6 +35,7 @@ TIE_INTEGER = 1
 VARIANT_AUTO = 0
 VARIANT_TABLE = 1
 VARIANT_FIELDWALK = 2
+VARIANT_COARSE = 3
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

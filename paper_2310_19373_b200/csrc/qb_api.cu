@@ -26,6 +26,7 @@
 #include "qb_table.cuh"
 #include "qb_batch.cuh"
 #include "qb_fieldwalk.cuh"
+#include "qb_coarse.cuh"
 
 namespace qb {
 
@@ -57,6 +58,8 @@ struct KernelSet {
   KFn search, mark, blocks, states, finalize;
   PFn prefix;
   KFn fieldwalk;  // per-step field-walk search kernel with the same blocks (big geometry only)
+  KFn coarse;     // packed-int16 filter search kernel with the same blocks (big geometry only)
+  std::atomic<int> occ_c{-1};
   std::atomic<int> occ_fw{-1};  // resident CTAs per SM for `fieldwalk` (lazy)
   std::atomic<int> occ{-1};  // resident CTAs per SM for `search` (lazy; shared by all devices)
 };
@@ -65,14 +68,21 @@ struct KernelSet {
   KernelSet {                                                                                            \
     B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB>, collect_mark_kernel<B1, B2, SB, L>,                \
         collect_blocks_kernel<B1, B2, SB, L>, collect_states_kernel<B1, B2, SB, L>,                      \
-        table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>, nullptr                 \
+        table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>, nullptr, nullptr        \
+  }
+#define QB_KSC(B1, B2, L)                                                                                \
+  KernelSet {                                                                                            \
+    B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
+        collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
+        table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>, nullptr,                  \
+        coarse_kernel<B1, B2, L, TPB>                                                                    \
   }
 #define QB_KSF(B1, B2, L)                                                                                \
   KernelSet {                                                                                            \
     B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
         collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
         table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>,                           \
-        fieldwalk_kernel<L, TPB>                                                                         \
+        fieldwalk_kernel<L, TPB>, coarse_kernel<B1, B2, L, TPB>                                          \
   }
 
 // Small problems (free bits < BIG_BE): one block of 2^L states per chunk, no sub-blocks.
@@ -87,7 +97,7 @@ struct KernelSet {
 constexpr int BIG_B1 = QB_BIG_B1, BIG_B2 = QB_BIG_B2, BIG_SB = QB_BIG_SB, BIG_BE = BIG_B1 + BIG_B2 + BIG_SB;
 static KernelSet g_sets[] = {
     QB_KS(0, 1, 0, 1),  QB_KS(1, 1, 0, 2),  QB_KS(1, 2, 0, 3),  QB_KS(2, 2, 0, 4),  QB_KS(2, 3, 0, 5),
-    QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KS(5, 5, 0, 10),
+    QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KSC(5, 5, 10),
 #if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB != 10
     QB_KS(BIG_B1, BIG_B2, BIG_SB, BIG_BE),
 #endif
@@ -124,7 +134,7 @@ struct Device {
   size_t chunk_min_cap = 0;
   unsigned long long* d_cand = nullptr;
   size_t cand_cap = 0;
-  unsigned long long* d_work = nullptr;
+  unsigned long long* d_work = nullptr;  // [0] chunk counter, [1] device-wide best (coarse kernel)
   unsigned long long* d_counts = nullptr;  // [0] chunks, [1] blocks, [2] candidates
   unsigned long long* h_counts = nullptr;  // pinned
   unsigned long long* d_lists = nullptr;   // chunk list | block list
@@ -159,7 +169,7 @@ static int get_device(Device** out) {
     QB_CUDA(cudaEventCreate(&d->evs));
     QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
     QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
-    QB_CUDA(cudaMalloc(&d->d_work, sizeof(unsigned long long)));
+    QB_CUDA(cudaMalloc(&d->d_work, 2 * sizeof(unsigned long long)));
     QB_CUDA(cudaMalloc(&d->d_counts, 3 * sizeof(unsigned long long)));
     QB_CUDA(cudaMallocHost(&d->h_counts, 3 * sizeof(unsigned long long)));
     QB_CUDA(cudaMalloc(&d->d_red, 2 * sizeof(unsigned long long)));
@@ -266,6 +276,22 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     }
   }
   for (int z = (1 << B); z < (1 << BMAX); ++z) P.T[z] = 0.f;
+  // coarse image for the filter kernel (qb_coarse.cuh): coarse unit 2^s quantized units, s the smallest
+  // shift with r_in * 2^-s + B + 2 <= 2^14 - 1, so every coarse component (subset sums of rounded
+  // fields, rounded table entries) fits a 15-bit field after the 2^14 bias
+  double rq_in = 0.0;
+  for (int i = 0; i < BE && i < n; ++i)
+    for (int j = i; j < n; ++j) rq_in += std::fabs(q[(size_t)i * n + j]);
+  int cs = 0;
+  while (std::ldexp(rq_in, -cs) + B + 2 > 16383.0) ++cs;
+  P.coarse_shift = cs;
+  P.coarse_scale = (float)std::ldexp(1.0, -cs);
+  const int bias = 1 << 14;
+  for (int z = 0; z < (1 << BMAX); z += 2) {
+    const int t0 = (z < (1 << B)) ? (int)std::nearbyint(std::ldexp((double)P.T[z], -cs)) : 0;
+    const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint(std::ldexp((double)P.T[z + 1], -cs)) : 0;
+    P.Tc2[z / 2] = (unsigned)(t0 + bias) | ((unsigned)(t1 + bias) << 16);
+  }
   return QB_OK;
 }
 
@@ -345,8 +371,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant != QB_VARIANT_AUTO && variant != QB_VARIANT_TABLE && variant != QB_VARIANT_FIELDWALK)
-    return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_COARSE) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -366,6 +391,12 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   pl.B = pl.ks->B1 + pl.ks->B2;
   // the field walk forms running values over all L free bits in fp32: bound every free bit
   const bool fieldwalk = variant == QB_VARIANT_FIELDWALK && pl.ks->fieldwalk != nullptr;
+  // the coarse filter pays off once each resident thread walks enough blocks for the running best to
+  // prune almost every block (>= 32 blocks per thread); small problems use the table kernel directly
+  const double blocks_per_thread =
+      std::ldexp(1.0, n - m_fix - BE) / (double)shard_count / ((double)dev->sms * QB_MINB * TPB);
+  const bool coarse = pl.ks->coarse != nullptr &&
+                      (variant == QB_VARIANT_COARSE || (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl)) return rc;
 
   TableParams& P = *pl.P;
@@ -383,7 +414,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   P.chunk_end = ce;
 
   std::memset(out, 0, sizeof(*out));
-  out->variant = fieldwalk ? QB_VARIANT_FIELDWALK : QB_VARIANT_TABLE;
+  out->variant = fieldwalk ? QB_VARIANT_FIELDWALK : (coarse ? QB_VARIANT_COARSE : QB_VARIANT_TABLE);
   out->scale_exp = pl.e;
   out->prefix_bits = pl.k;
   out->exact = pl.exact ? 1 : 0;
@@ -398,8 +429,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
 
   KernelSet& ks = *pl.ks;
-  const KFn search_fn = fieldwalk ? ks.fieldwalk : ks.search;
-  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : ks.occ;
+  const KFn search_fn = fieldwalk ? ks.fieldwalk : (coarse ? ks.coarse : ks.search);
+  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : (coarse ? ks.occ_c : ks.occ);
   int occ = occ_cache.load();
   if (occ < 0) {
     int o = 0;
@@ -414,6 +445,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   P.cta_out = dev->d_cta;
   P.final_out = dev->d_final;
   P.work = dev->d_work;
+  P.gbest = reinterpret_cast<long long*>(dev->d_work + 1);
   P.nrec = grid;
   const bool collect = !pl.exact || all_out != nullptr;
   P.mode = collect ? MODE_SEARCH_RECORD : MODE_SEARCH;
@@ -434,6 +466,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   cudaStream_t st = dev->stream;
   QB_CUDA(cudaMemsetAsync(dev->d_work, 0, sizeof(unsigned long long), st));
+  QB_CUDA(cudaMemsetAsync(dev->d_work + 1, 0x7f, sizeof(unsigned long long), st));  // "+infinity"
   QB_CUDA(cudaEventRecord(dev->ev0, st));
   search_fn<<<grid, TPB, 0, st>>>(P);
   QB_CUDA(cudaGetLastError());

@@ -1,0 +1,150 @@
+// Coarse-filter traversal kernel (default for large chunks): packed int16 block pass + exact
+// fp32 re-evaluation of the blocks that could beat or tie the running best.
+//
+// Same chunks, outer Gray walk (Eq. 3 field updates), blocks and tie keys as the table kernel
+// (qb_table.cuh).  Each 1024-state block is first evaluated in a coarse integer image:
+//     hc_i = rint(H_i * 2^-s),  Tc(z) = rint(T(z) * 2^-s),  C(z) = sum_{i in z} hc_i + Tc(z)
+// with two states per 32-bit register (biased 16-bit fields, see below): one 32-bit add forms a
+// pair of candidates, VIMNMX3.U16x2 folds two pairs into the running pair-minimum — about one
+// instruction per state, table operands from uniform registers.  s is chosen on the host so
+// that every coarse component fits a biased 15-bit field.  Each hc_i and Tc(z) carries at most half a coarse unit of rounding, so
+//     exact(z) >= (C(z) - (B+1)/2) * 2^s      (certified lower bound, quantized units)
+// A block whose bound exceeds the thread's best value cannot contain a better or tied state and is
+// skipped; otherwise its exact minimum comes from the fp32 table evaluation (rare after the first
+// blocks of a thread).  When s = 0 the coarse image is exact and no re-evaluation is needed.
+// The per-chunk minima written for the certified collect pass are lower bounds (exact for
+// evaluated blocks, the coarse bound for skipped ones), which keeps that pass complete.
+#pragma once
+#include "qb_table.cuh"
+
+namespace qb {
+
+// Packed coarse pairs: two 16-bit fields per 32-bit register, each biased by 2^14 so that a
+// plain 32-bit add of two packed values (both fields in [0, 2^15)) never carries between fields.
+// The adds are ordinary VIADD / IADD3 that take the table operand straight from a uniform register
+// (LDCU.128 = 8 states, broadcast through the operand path, not replicated per lane), and
+// VIMNMX3.U16x2 folds two candidate pairs into the running pair-minimum (4 states per min).
+constexpr int CB = 1 << 14;  // field bias
+
+__device__ __forceinline__ unsigned umin2(unsigned a, unsigned b) {
+  unsigned r;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned umin3(unsigned a, unsigned b, unsigned c) { return umin2(umin2(a, b), c); }
+
+// Coarse minimum over the 2^B states of a block, in coarse units (exact integer arithmetic).
+template <int B1, int B2>
+__device__ __forceinline__ int coarse_block_min(const TableParams& p, const float (&H)[B1 + B2]) {
+  constexpr int B = B1 + B2, NU = 1 << B1, NP = 1 << (B2 - 1);
+  static_assert(B2 >= 3, "pairs of w, four pairs per table load");
+  int hc[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) hc[i] = __float2int_rn(H[i] * p.coarse_scale);
+  // Bw2[m] = (Bw(2m) + 2^14) | (Bw(2m+1) + 2^14) << 16, Bw(w) = sum_{i in w} hc_i
+  unsigned Bw2[NP];
+  Bw2[0] = (unsigned)CB + ((unsigned)(CB + hc[0]) << 16);
+#pragma unroll
+  for (int i = 1; i < B2; ++i) {
+    const unsigned d = (unsigned)hc[i] * 0x10001u;  // adds hc_i to both fields (no carry: fields stay in range)
+#pragma unroll
+    for (int m = 0; m < (1 << (i - 1)); ++m) Bw2[m + (1 << (i - 1))] = Bw2[m] + d;
+  }
+  // A[u] = sum_{i in u} hc_{B2+i} - 2^15 (removes the two field biases of a candidate)
+  int A[NU];
+  A[0] = -2 * CB;
+#pragma unroll
+  for (int i = 0; i < B1; ++i)
+#pragma unroll
+    for (int u = 0; u < (1 << i); ++u) A[u + (1 << i)] = A[u] + hc[B2 + i];
+  int rmin = 0;
+#pragma unroll
+  for (int u = 0; u < NU; u += 2) {
+    int r[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      unsigned acc2 = 0u;
+#pragma unroll
+      for (int m = 0; m < NP; m += 4) {
+        const uint4 t = *reinterpret_cast<const uint4*>(&p.Tc2[(u + h) * NP + m]);
+        const unsigned c0 = Bw2[m] + t.x, c1 = Bw2[m + 1] + t.y;
+        const unsigned c2 = Bw2[m + 2] + t.z, c3 = Bw2[m + 3] + t.w;
+        acc2 = (m == 0) ? umin2(c0, c1) : umin3(acc2, c0, c1);
+        acc2 = umin3(acc2, c2, c3);
+      }
+      r[h] = (int)min(acc2 & 0xffffu, acc2 >> 16) + A[u + h];
+    }
+    rmin = (u == 0) ? min(r[0], r[1]) : min(min(rmin, r[0]), r[1]);
+  }
+  return rmin;
+}
+
+template <int B1, int B2, int L, int TPB>
+__global__ void __launch_bounds__(TPB, QB_MINB) coarse_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2;
+  constexpr int LO = L - B;
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+  const int lane = threadIdx.x & 31;
+  const long long slack = (long long)(B + 1) << p.coarse_shift >> 1;  // (B+1)/2 coarse units, quantized
+  const bool coarse_exact = p.coarse_shift == 0;
+
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(p.work, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= nchunks) break;
+    const unsigned long long ci = base + lane;
+    if (ci >= nchunks) continue;
+    const unsigned long long c = p.chunk_begin + ci;
+    const unsigned long long s = chunk_prefix(p, c);
+    long long V;
+    float H[B], F[NF];
+    base_eval<B, L>(p, s << L, L, V, H, F);
+    int dir;
+    const unsigned long long key_hi = chunk_key(p, s, dir);
+    long long cmin = LLONG_MAX;
+    // pruning threshold: the better of this thread's best and the device-wide best so far (any
+    // block whose bound exceeds a value some state attains holds neither a minimiser nor a tie)
+    long long thr = min(best.val, __ldcg(p.gbest));
+    for (unsigned int j = 0; j < (1u << LO); ++j) {
+      if (j) {
+        const int r = __ffs(j) - 1;
+        const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
+        outer_flip<B, L, B>(p, B + r, sg, V, H, F);
+      }
+      // device-wide best: short chunks (<= 64 blocks) refresh it every block, long chunks only at
+      // the chunk start (measured: the per-block load costs ~5% at 1024 blocks per chunk)
+      long long gb = LLONG_MAX;
+      if constexpr (LO <= 6) gb = __ldcg(p.gbest);
+      const long long cb = V + ((long long)coarse_block_min<B1, B2>(p, H) << p.coarse_shift);
+      thr = min(thr, gb);
+      long long val;
+      if (coarse_exact) {
+        val = cb;
+      } else {
+        const long long lb = cb - slack;
+        if (lb > thr) {  // no state of this block can beat or tie the best value seen
+          cmin = min(cmin, lb);
+          continue;
+        }
+        val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
+      }
+      cmin = min(cmin, val);
+      if (val <= best.val) {
+        const unsigned long long K = block_key(p, key_hi, dir, j, LO);
+        if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
+        if (val < thr) {
+          thr = val;
+          atomicMin(p.gbest, val);
+        }
+      }
+    }
+    if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
+  }
+  const Rec r = cta_reduce<TPB>(best);
+  if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
+}
+
+}  // namespace qb

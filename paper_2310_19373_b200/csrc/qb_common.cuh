@@ -42,6 +42,9 @@ struct alignas(16) TableParams {
   float T[1 << BMAX];        // inner table: T[z] = sum_{i<=j<B} q_ij z_i z_j, z = (u << B2) | w
   float Qs[NMAX][NMAX];      // quantized symmetric off-diagonal part (0 on the diagonal)
   float d[NMAX];             // quantized diagonal
+  unsigned Tc2[1 << (BMAX - 1)];  // coarse table pairs: Tc2[z/2] = (Tc(z) + 2^14) | (Tc(z+1) + 2^14) << 16
+  float coarse_scale;        // 2^-s: coarse units per quantized unit
+  int coarse_shift;          // s (coarse unit = 2^s quantized units); 0 = coarse is exact
   int n, k, L, m_fix;
   int m_tie, rule, mode, nrec;
   unsigned long long suffix;       // value of the m_fix fixed high bits
@@ -55,6 +58,7 @@ struct alignas(16) TableParams {
   Rec* cta_out;                    // one record per CTA
   FinalOut* final_out;
   unsigned long long* work;        // dynamic chunk counter (zeroed before each search launch)
+  long long* gbest;                // device-wide best value so far (coarse kernel pruning threshold)
   unsigned long long* counts;      // collect pass counters: [0] chunks, [1] blocks, [2] unused
   unsigned long long* chunk_list;  // chunk offsets (c - chunk_begin) whose minimum is <= theta
   unsigned long long* block_list;  // (chunk offset << 32) | block j, block minimum <= theta

@@ -140,10 +140,15 @@ def test_sharding_is_invariant():
 
 def test_config_e_n40_properties():
     """n=40 is beyond the oracle: check the argmin against exact CPU scans of the
-    subspace that contains it and of random other subspaces."""
+    subspace that contains it and of random other subspaces; the default (coarse-filter)
+    kernel, the fp32 table kernel and the field walk agree."""
     c = instances.config_coeffs("E", 0)
     inst = qb.QuboInstance(c)
     sol = qb.solve_incremental(inst)
+    auto = _lib.solve(c)
+    assert auto.variant == _lib.VARIANT_COARSE
+    table = _lib.solve(c, variant=_lib.VARIANT_TABLE)
+    assert (auto.argmin_bits, auto.value, auto.tie_key) == (table.argmin_bits, table.value, table.tie_key)
     x = _bits(sol)
     assert sol.value == O.eval_upper(c, sol.minimizer.astype(np.float64))
     m = 17  # 2^23-state subspaces
@@ -351,3 +356,18 @@ def test_adversarial_value_ranges_vs_oracle(kind):
             bits, val, _ = O.solve_subspaces(inst.coeffs, m)
             sol = qb.solve_parallel(inst, qb.SolveConfig(threads=2, fixed_bits=m))
             assert (_bits(sol), sol.value) == (bits, val), (kind, n, seed, m)
+
+
+@pytest.mark.parametrize("n", [31, 33])
+def test_coarse_kernel_matches_table_kernel(n):
+    """The packed-int16 filter kernel (default for large chunks) returns exactly what the fp32
+    table kernel returns: integer and float instances, tie-heavy instances, subspaces, tie rules."""
+    cases = [instances.config_coeffs("D", 9, n=n), instances.config_coeffs("E", 9, n=n),
+             instances.config_coeffs("B", 9, n=n), _tie_heavy(n, 4100 + n, -1, 1),
+             instances.int_uniform_coeffs(n, 4200 + n, -(1 << 20), 1 << 20)]
+    for c in cases:
+        for args in ((0, 0, 0), (0, 0, 4), (3, 5, 3)):
+            a = _lib.solve(c, *args, variant=_lib.VARIANT_TABLE)
+            b = _lib.solve(c, *args, variant=_lib.VARIANT_COARSE)
+            assert b.variant == _lib.VARIANT_COARSE  # chunks of >= 10 free bits have a coarse kernel
+            assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (n, args)

@@ -33,13 +33,15 @@ __device__ __forceinline__ long long clk() {
   return c;
 }
 
-enum { K_FADD, K_FADD2, K_FFMA, K_FMNMX3, K_DADD, K_IADD3, K_VIMNMX3, K_MIX, K_NK };
+enum { K_FADD, K_FADD2, K_FFMA, K_FMNMX3, K_DADD, K_IADD3, K_VIMNMX3, K_MIX, K_VIADD16, K_VMIN3_16, K_MIX16, K_NK };
 static const char* NAMES[K_NK] = {"fadd", "fadd2", "ffma", "fmnmx3", "dadd", "iadd3", "vimnmx3",
-                                  "mix_fadd2_fmnmx3_ldcu128"};
+                                  "mix_fadd2_fmnmx3_ldcu128", "viadd_16x2", "vimnmx3_s16x2",
+                                  "mix16_viadd2_vimnmx3_ldcu128"};
 // lane-operations per instruction: FADD2 / IADD3 = 2 adds, FMNMX3 / VIMNMX3 = 2 two-input mins,
 // MIX counts states (one FADD2 + one FMNMX3 per 2 states)
-static const double OPS[K_NK] = {1, 2, 1, 2, 1, 2, 2, 2};
-static const int INSTR_PER_ITER[K_NK] = {CH, CH / 2, CH, CH, CH, CH, CH, CH / 2};
+static const double OPS[K_NK] = {1, 2, 1, 2, 1, 2, 2, 2, 2, 4, 2};
+// MIX16 per iteration: 8 VIADD.16x2 (16 states) + 4 VIMNMX3.S16x2; counted as 8 "instructions" of 2 states
+static const int INSTR_PER_ITER[K_NK] = {CH, CH / 2, CH, CH, CH, CH, CH, CH / 2, CH, CH, CH / 2};
 
 struct Tab {
   float t[2048];
@@ -58,6 +60,36 @@ __global__ void __launch_bounds__(TPB, 2) kern(const __grid_constant__ Tab tab, 
       for (int i = 0; i < CH; i++) asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(d[i]) : "d"(d[(i + 1) % CH]));
 #pragma unroll
     for (int i = 0; i < CH; i++) acc += (float)d[i];
+  } else if constexpr (K == K_VIADD16 || K == K_VMIN3_16 || K == K_MIX16) {
+    unsigned v[CH];
+#pragma unroll
+    for (int i = 0; i < CH; i++) v[i] = threadIdx.x * (i + 3);
+    for (int it = 0; it < ITERS; it++) {
+      if constexpr (K == K_VIADD16) {
+#pragma unroll
+        for (int i = 0; i < CH; i++) asm volatile("add.s16x2 %0, %0, %1;" : "+r"(v[i]) : "r"(v[(i + 1) % CH]));
+      } else if constexpr (K == K_VMIN3_16) {
+#pragma unroll
+        for (int i = 0; i < CH; i++)
+          asm volatile("{ .reg .b32 t; min.s16x2 t, %0, %1; min.s16x2 %0, t, %2; }" : "+r"(v[i]) : "r"(v[(i + 1) % CH]), "r"(v[(i + 2) % CH]));
+      } else {
+        // packed-int16 table loop: c = B pair + T pair (constant bank), acc = min3(acc, c0, c1)
+        const int base = (it & 1) * 1024;
+#pragma unroll
+        for (int i = 0; i < CH; i += 4) {
+          const uint4 t = *reinterpret_cast<const uint4*>(&tab.t[base + 2 * i]);
+          unsigned c0, c1;
+          asm("add.s16x2 %0, %1, %2;" : "=r"(c0) : "r"(v[i]), "r"(t.x));
+          asm("add.s16x2 %0, %1, %2;" : "=r"(c1) : "r"(v[i + 1]), "r"(t.y));
+          asm volatile("{ .reg .b32 m; min.s16x2 m, %0, %1; min.s16x2 %0, m, %2; }" : "+r"(v[i + 2]) : "r"(c0), "r"(c1));
+          asm("add.s16x2 %0, %1, %2;" : "=r"(c0) : "r"(v[i + 1]), "r"(t.z));
+          asm("add.s16x2 %0, %1, %2;" : "=r"(c1) : "r"(v[i]), "r"(t.w));
+          asm volatile("{ .reg .b32 m; min.s16x2 m, %0, %1; min.s16x2 %0, m, %2; }" : "+r"(v[i + 3]) : "r"(c0), "r"(c1));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CH; i++) acc += (float)(v[i] & 0xffff);
   } else if constexpr (K == K_IADD3 || K == K_VIMNMX3) {
     int v[CH];
 #pragma unroll
@@ -175,6 +207,9 @@ int main() {
   run<K_IADD3>(sms, dout, dcyc, tab, false);
   run<K_VIMNMX3>(sms, dout, dcyc, tab, false);
   run<K_MIX>(sms, dout, dcyc, tab, false);
+  run<K_VIADD16>(sms, dout, dcyc, tab, false);
+  run<K_VMIN3_16>(sms, dout, dcyc, tab, false);
+  run<K_MIX16>(sms, dout, dcyc, tab, false);
   printf("}}\n");
   return 0;
 }
