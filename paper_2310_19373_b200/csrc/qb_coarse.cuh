@@ -25,6 +25,24 @@ namespace qb {
 // (LDCU.128 = 8 states, broadcast through the operand path, not replicated per lane), and
 // VIMNMX3.U16x2 folds two candidate pairs into the running pair-minimum (4 states per min).
 constexpr int CB = 1 << 14;  // field bias
+#ifndef QB_COARSE_ROLLED
+#define QB_COARSE_ROLLED 0  // 1: rolled row loop (measured slower: runtime table addresses become per-thread LDCs)
+#endif
+#ifndef QB_EXACT_NOINLINE
+#define QB_EXACT_NOINLINE 1  // long chunks call the exact re-evaluation out of line (measured n=40: 52 -> 41 ms)
+#endif
+
+// exact fp32 re-evaluation of one block, out of line (rare path: keeps its 64 live table-loop
+// registers out of the coarse loop's allocation)
+template <int B1, int B2, int NF>
+__device__ __noinline__ float exact_block_min_ool(const TableParams& p, const float* Hp, const float* Fp) {
+  float H[B1 + B2], F[NF];
+#pragma unroll
+  for (int i = 0; i < B1 + B2; ++i) H[i] = Hp[i];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) F[i] = Fp[i];
+  return block_min<B1, B2, 0, NF>(p, H, F);
+}
 
 __device__ __forceinline__ unsigned umin2(unsigned a, unsigned b) {
   unsigned r;
@@ -50,6 +68,34 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
 #pragma unroll
     for (int m = 0; m < (1 << (i - 1)); ++m) Bw2[m + (1 << (i - 1))] = Bw2[m] + d;
   }
+#if QB_COARSE_ROLLED
+  // rows in a rolled loop over row pairs (u0 = 2g, u0 + 1): the uniform table address depends on g,
+  // which bounds how far ptxas can hoist the LDCU.128 loads (unrolled, it exhausts the 63 uniform
+  // registers and spills); A_u from the bits of g with predicated adds
+  int rmin = INT_MAX;
+#pragma unroll 1
+  for (int g = 0; g < NU / 2; ++g) {
+    int Ag = -2 * CB;
+#pragma unroll
+    for (int i = 1; i < B1; ++i) Ag += ((g >> (i - 1)) & 1) ? hc[B2 + i] : 0;
+    const unsigned* trow = &p.Tc2[(2 * g) * NP];
+    int r[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      unsigned acc2 = 0u;
+#pragma unroll
+      for (int m = 0; m < NP; m += 4) {
+        const uint4 t = *reinterpret_cast<const uint4*>(trow + h * NP + m);
+        const unsigned c0 = Bw2[m] + t.x, c1 = Bw2[m + 1] + t.y;
+        const unsigned c2 = Bw2[m + 2] + t.z, c3 = Bw2[m + 3] + t.w;
+        acc2 = (m == 0) ? umin2(c0, c1) : umin3(acc2, c0, c1);
+        acc2 = umin3(acc2, c2, c3);
+      }
+      r[h] = (int)min(acc2 & 0xffffu, acc2 >> 16) + Ag + (h ? hc[B2] : 0);
+    }
+    rmin = min(min(rmin, r[0]), r[1]);
+  }
+#else
   // A[u] = sum_{i in u} hc_{B2+i} - 2^15 (removes the two field biases of a candidate)
   int A[NU];
   A[0] = -2 * CB;
@@ -76,6 +122,7 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
     }
     rmin = (u == 0) ? min(r[0], r[1]) : min(min(rmin, r[0]), r[1]);
   }
+#endif
   return rmin;
 }
 
@@ -129,7 +176,10 @@ __global__ void __launch_bounds__(TPB, QB_MINB) coarse_kernel(const __grid_const
           cmin = min(cmin, lb);
           continue;
         }
-        val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
+        // short chunks (<= 64 blocks) re-evaluate often enough that inlining wins; long chunks call
+        // out of line so the coarse loop keeps the registers
+        if constexpr (QB_EXACT_NOINLINE && LO > 6) val = V + (long long)exact_block_min_ool<B1, B2, NF>(p, H, F);
+        else val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
       }
       cmin = min(cmin, val);
       if (val <= best.val) {
