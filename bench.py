@@ -47,7 +47,7 @@ ALU_PEAKS = os.path.join(ROOT, "profiles", "r01_alu_peaks.json")
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
 # SASS instructions per state of the table kernel's inner block (cuobjdump count)
-SASS_INSTR_PER_STATE = 1.48  # ncu smsp__inst_executed x 32 / 2^40 (profiles/r02_ncu_search_summary.txt)
+SASS_INSTR_PER_STATE = 1.20  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r03_ncu_search_summary.txt)
 
 
 def parse():
@@ -355,17 +355,18 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_extra:
         line["configs"] = extra_configs(qb, _lib, instances)
-        # the literal per-step field-walk kernel (QB_VARIANT_FIELDWALK) on the same workload
-        _lib.solve(inst.coeffs, variant=_lib.VARIANT_FIELDWALK)
-        fw = _lib.solve(inst.coeffs, variant=_lib.VARIANT_FIELDWALK)
-        fw_states_s = states / (fw.search_ms * 1e-3)
-        line["variants"] = {
-            "table": {"search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s},
-            "fieldwalk": {"search_ms": fw.search_ms, "states_per_s": fw_states_s,
-                          "nominal_roofline_frac": fw_states_s * (n + 1) / peak,
-                          "same_argmin": int(fw.argmin_bits) == int(r.argmin_bits),
-                          "variant_used": int(fw.variant)},
-        }
+        # the other traversal kernels on the same workload: the fp32 table kernel and the literal
+        # per-step field walk (QB_VARIANT_TABLE / QB_VARIANT_FIELDWALK)
+        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse"}
+        line["variants"] = {f"{names[int(r.variant)]} (default)": {
+            "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
+        for var in (_lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK):
+            _lib.solve(inst.coeffs, variant=var)
+            vr = _lib.solve(inst.coeffs, variant=var)
+            vs = states / (vr.search_ms * 1e-3)
+            line["variants"][names[var]] = {"search_ms": vr.search_ms, "states_per_s": vs,
+                                           "nominal_roofline_frac": vs * (n + 1) / peak,
+                                           "same_argmin": int(vr.argmin_bits) == int(r.argmin_bits)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_sample(inst.coeffs, args.cpu_seconds)
         cb.pop("seconds", None)

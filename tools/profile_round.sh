@@ -9,6 +9,6 @@ python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-extra > gpurun_out/b
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-extra > gpurun_out/ncu_launch_$tag.log 2>&1
 python tools/profile_case.py E > gpurun_out/prof_plain_$tag.log 2>&1 && \
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:qb::table_kernel<" -s 1 -c 1 -o gpurun_out/prof_search_$tag python tools/profile_case.py E \
+    -k "regex:qb::coarse_kernel<" -s 1 -c 1 -o gpurun_out/prof_search_$tag python tools/profile_case.py E \
     > gpurun_out/ncu_full_$tag.log 2>&1
 cat gpurun_out/bench_$tag.json
