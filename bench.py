@@ -46,6 +46,24 @@ CONFIG_DESC = {
 ALU_PEAKS = os.path.join(ROOT, "profiles", "r01_alu_peaks.json")
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
+# ncu --set full capture of the search kernel (DRAM bytes per launch, n=40 config E)
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r03_ncu_search_summary.txt")
+
+
+def ncu_traffic_bytes():
+    """dram__bytes_read.sum + dram__bytes_write.sum (MB in the summary) -> bytes, or None."""
+    try:
+        vals = {}
+        with open(NCU_SUMMARY) as fh:
+            for line in fh:
+                if line.startswith("dram__bytes_read.sum =") or line.startswith("dram__bytes_write.sum ="):
+                    k, v = line.split("=")
+                    vals[k.strip()] = float(v) * 1e6
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # SASS instructions per state of the table kernel's inner block (cuobjdump count, DESIGN.md §4)
 SASS_INSTR_PER_STATE = 1.20  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r03_ncu_search_summary.txt)
 
@@ -327,7 +345,9 @@ def main():
     issue_peak = ISSUE_WARP_INSTR_PER_SM_CLK * 32 * sm_count * sm_hz
     roofline = {
         "bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
-        "frac": achieved / peak, "traffic": None,
+        "frac": achieved / peak, "traffic": ncu_traffic_bytes(),
+        "traffic_note": "DRAM bytes per search launch from the committed ncu capture (profiles/r03_ncu_search_summary.txt, "
+                        "n=40): the per-chunk minima and CTA records; the algorithmic HBM traffic per state is 0",
         "basis": f"nominal {n + 1} ops/state (SURVEY.md §8d: n-1 field adds + 1 value add + 1 min) vs the "
                  f"{peak_src}; the table kernel issues ~{SASS_INSTR_PER_STATE} SASS instr/state, so frac > 1 "
                  "measures the algorithmic saving and issue_frac (vs 4 warp-instr/SM/clk) the kernel quality",
