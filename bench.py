@@ -51,14 +51,16 @@ NCU_SUMMARY = os.path.join(ROOT, "profiles", "r03_ncu_search_summary.txt")
 
 
 def ncu_traffic_bytes():
-    """dram__bytes_read.sum + dram__bytes_write.sum (MB in the summary) -> bytes, or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum of the committed capture, in bytes, or None."""
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     try:
         vals = {}
         with open(NCU_SUMMARY) as fh:
             for line in fh:
                 if line.startswith("dram__bytes_read.sum =") or line.startswith("dram__bytes_write.sum ="):
-                    k, v = line.split("=")
-                    vals[k.strip()] = float(v) * 1e6
+                    k, rest = line.split("=")
+                    num, unit = rest.split()
+                    vals[k.strip()] = float(num) * scale[unit]
         return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
     except (OSError, KeyError, ValueError):
         return None

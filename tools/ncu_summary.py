@@ -6,7 +6,7 @@ rep = sys.argv[1]
 states = float(sys.argv[2]) if len(sys.argv) > 2 else 2.0 ** 40
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
-h, v = r[0], r[2]
+h, units, v = r[0], r[1], r[2]
 want = ["Kernel Name", "gpu__time_duration.sum", "launch__registers_per_thread", "launch__occupancy_limit_registers",
         "launch__grid_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
@@ -16,12 +16,13 @@ want = ["Kernel Name", "gpu__time_duration.sum", "launch__registers_per_thread",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__cycles_elapsed.avg.per_second",
         "smsp__warps_eligible.avg.per_cycle_active"]
 out = {}
-for k, x in zip(h, v):
+for k, un, x in zip(h, units, v):
     if k in want:
-        out[k] = x
+        out[k] = (x, un)
 for k in want:
     if k in out:
-        print(f"{k} = {out[k]}")
+        x, un = out[k]
+        print(f"{k} = {x}" + (f" {un}" if un else ""))
 print("-- stall reasons (per issue):")
 for k, x in zip(h, v):
     if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
