@@ -371,3 +371,17 @@ def test_coarse_kernel_matches_table_kernel(n):
             b = _lib.solve(c, *args, variant=_lib.VARIANT_COARSE)
             assert b.variant == _lib.VARIANT_COARSE  # chunks of >= 10 free bits have a coarse kernel
             assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (n, args)
+
+
+@pytest.mark.parametrize("kind", ["big_int", "wide_range", "tiny", "neg_zero", "dyadic"])
+def test_adversarial_value_ranges_coarse_kernel(kind):
+    """The coarse kernel's int16 image (scale shift, bias, certified slack) on adversarial value
+    ranges at n=30, against the fp32 table kernel (itself checked against the oracle)."""
+    for seed in range(2):
+        c = _adversarial(kind, 30, 7000 + seed)
+        inst = qb.QuboInstance(c)
+        for args in ((0, 0, 0), (0, 0, 5)):
+            a = _lib.solve(inst.coeffs, *args, variant=_lib.VARIANT_TABLE)
+            b = _lib.solve(inst.coeffs, *args, variant=_lib.VARIANT_COARSE)
+            assert b.variant == _lib.VARIANT_COARSE
+            assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (kind, seed, args)
