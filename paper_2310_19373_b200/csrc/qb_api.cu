@@ -75,14 +75,14 @@ struct KernelSet {
     B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
         collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
         table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>, nullptr,                  \
-        coarse_kernel<B1, B2, L, TPB>                                                                    \
+        coarse_kernel<B1, B2, QB_COARSE_B1, QB_COARSE_B2, L, TPB>                                        \
   }
 #define QB_KSF(B1, B2, L)                                                                                \
   KernelSet {                                                                                            \
     B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
         collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
         table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>,                           \
-        fieldwalk_kernel<L, TPB>, coarse_kernel<B1, B2, L, TPB>                                          \
+        fieldwalk_kernel<L, TPB>, coarse_kernel<B1, B2, QB_COARSE_B1, QB_COARSE_B2, L, TPB>              \
   }
 
 // Small problems (free bits < BIG_BE): one block of 2^L states per chunk, no sub-blocks.
@@ -94,16 +94,21 @@ struct KernelSet {
 #ifndef QB_BIG_SB
 #define QB_BIG_SB 0
 #endif
+#ifndef QB_COARSE_B1  // coarse pass split of the 10 table bits: u rows x w columns (measured best 4 x 6)
+#define QB_COARSE_B1 4
+#define QB_COARSE_B2 6
+#endif
 constexpr int BIG_B1 = QB_BIG_B1, BIG_B2 = QB_BIG_B2, BIG_SB = QB_BIG_SB, BIG_BE = BIG_B1 + BIG_B2 + BIG_SB;
 static KernelSet g_sets[] = {
     QB_KS(0, 1, 0, 1),  QB_KS(1, 1, 0, 2),  QB_KS(1, 2, 0, 3),  QB_KS(2, 2, 0, 4),  QB_KS(2, 3, 0, 5),
-    QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KSC(5, 5, 10),
+    QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KSC(BIG_B1, BIG_B2, 10),
 #if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB != 10
     QB_KS(BIG_B1, BIG_B2, BIG_SB, BIG_BE),
 #endif
 #if QB_BIG_SB == 0 && QB_BIG_B1 + QB_BIG_B2 == 10
-    QB_KSF(5, 5, 11), QB_KSF(5, 5, 12), QB_KSF(5, 5, 13), QB_KSF(5, 5, 14), QB_KSF(5, 5, 16), QB_KSF(5, 5, 18),
-    QB_KSF(5, 5, 20), QB_KSF(5, 5, 22),
+    QB_KSF(BIG_B1, BIG_B2, 11), QB_KSF(BIG_B1, BIG_B2, 12), QB_KSF(BIG_B1, BIG_B2, 13), QB_KSF(BIG_B1, BIG_B2, 14),
+    QB_KSF(BIG_B1, BIG_B2, 16), QB_KSF(BIG_B1, BIG_B2, 18),
+    QB_KSF(BIG_B1, BIG_B2, 20), QB_KSF(BIG_B1, BIG_B2, 22),
 #else
 #if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB < 11
     QB_KS(BIG_B1, BIG_B2, BIG_SB, 11),

@@ -126,9 +126,12 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
   return rmin;
 }
 
-template <int B1, int B2, int L, int TPB>
+// (B1, B2): the fp32 table split used by the exact fallback; (CB1, CB2): the coarse pass's own split
+// of the same B table bits (both index the table as z = (u << B2) | w over the same bits).
+template <int B1, int B2, int CB1, int CB2, int L, int TPB>
 __global__ void __launch_bounds__(TPB, QB_MINB) coarse_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
+  static_assert(CB1 + CB2 == B, "coarse split must cover the table bits");
   constexpr int LO = L - B;
   constexpr int NF = (L - B) > 0 ? (L - B) : 1;
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(TPB, QB_MINB) coarse_kernel(const __grid_const
       // the chunk start (measured: the per-block load costs ~5% at 1024 blocks per chunk)
       long long gb = LLONG_MAX;
       if constexpr (LO <= 6) gb = __ldcg(p.gbest);
-      const long long cb = V + ((long long)coarse_block_min<B1, B2>(p, H) << p.coarse_shift);
+      const long long cb = V + ((long long)coarse_block_min<CB1, CB2>(p, H) << p.coarse_shift);
       thr = min(thr, gb);
       long long val;
       if (coarse_exact) {
