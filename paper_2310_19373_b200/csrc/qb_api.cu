@@ -288,10 +288,15 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
   for (int i = 0; i < BE && i < n; ++i)
     for (int j = i; j < n; ++j) rq_in += std::fabs(q[(size_t)i * n + j]);
   int cs = 0;
-  while (std::ldexp(rq_in, -cs) + B + 2 > 16383.0) ++cs;
+#if QB_PACKED_ROWS
+  const double field_max = 8191.0;
+#else
+  const double field_max = 16383.0;
+#endif
+  while (std::ldexp(rq_in, -cs) + B + 2 > field_max) ++cs;
   P.coarse_shift = cs;
   P.coarse_scale = (float)std::ldexp(1.0, -cs);
-  const int bias = 1 << 14;
+  const int bias = (int)field_max + 1;
   for (int z = 0; z < (1 << BMAX); z += 2) {
     const int t0 = (z < (1 << B)) ? (int)std::nearbyint(std::ldexp((double)P.T[z], -cs)) : 0;
     const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint(std::ldexp((double)P.T[z + 1], -cs)) : 0;
