@@ -163,8 +163,12 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
 
 // (B1, B2): the fp32 table split used by the exact fallback; (CB1, CB2): the coarse pass's own split
 // of the same B table bits (both index the table as z = (u << B2) | w over the same bits).
+#ifndef QB_COARSE_MINB
+#define QB_COARSE_MINB 4  // 128 registers: fewer uniform-register spills beat the fifth CTA (measured)
+#endif
+
 template <int B1, int B2, int CB1, int CB2, int L, int TPB>
-__global__ void __launch_bounds__(TPB, QB_MINB) coarse_kernel(const __grid_constant__ TableParams p) {
+__global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(CB1 + CB2 == B, "coarse split must cover the table bits");
   constexpr int LO = L - B;
