@@ -19,7 +19,8 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("QB_LIB_PATH") or os.path.join(PKG_DIR, "libqubrute_b200.so")
 HEADER = os.path.join(REPO_DIR, "include", "qubrute_b200.h")
-SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("qb_api.cu",)]
+SOURCES = [os.path.join(PKG_DIR, "csrc", f)
+           for f in ("qb_api.cu", "qb_k_table.cu", "qb_k_coarse.cu", "qb_k_fieldwalk.cu", "qb_k_batch.cu")]
 DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]
 
 QB_OK = 0
@@ -96,17 +97,34 @@ _lock = threading.Lock()
 _lib = None
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libqubrute_b200.so in-tree for sm_100a (skipped when up to date)."""
-    if not force and os.path.exists(LIB_PATH):
-        mtime = os.path.getmtime(LIB_PATH)
+def build(force: bool = False, verbose: bool = False, output: str | None = None, defines=()) -> str:
+    """Compile libqubrute_b200.so in-tree for sm_100a (skipped when up to date).
+
+    Each translation unit (host runtime + one per kernel family) is compiled by its own nvcc
+    process in parallel, then linked with ``nvcc -shared``.  ``output`` / ``defines`` build an
+    experimental variant elsewhere (tools/build_variants.sh)."""
+    out = output or LIB_PATH
+    if not force and output is None and os.path.exists(out):
+        mtime = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= mtime for d in DEPS if os.path.exists(d)):
-            return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
-    return LIB_PATH
+            return out
+    objdir = os.path.join(REPO_DIR, "build", "obj", os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(defines)
+    procs = []
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        cmd = ["nvcc", *compile_flags, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        procs.append((src, subprocess.Popen(cmd)))
+        objs.append(obj)
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {failed}")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs], check=True)
+    return out
 
 
 def lib():

@@ -23,10 +23,7 @@
 
 #include "../../include/qubrute_b200.h"
 #include "qb_common.cuh"
-#include "qb_table.cuh"
-#include "qb_batch.cuh"
-#include "qb_fieldwalk.cuh"
-#include "qb_coarse.cuh"
+#include "qb_registry.h"
 
 namespace qb {
 
@@ -46,82 +43,48 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 // ------------------------------------------------------------------ kernel registry
-#ifndef QB_TPB
-#define QB_TPB 128
-#endif
-constexpr int TPB = QB_TPB;
-using KFn = void (*)(const TableParams);
-using PFn = void (*)(const TableParams, double*, double*, int);
-
+// One entry per block shape / chunk length: the table family (qb_k_table.cu) plus, on the
+// large-block geometry, the coarse (qb_k_coarse.cu) and field-walk (qb_k_fieldwalk.cu) search
+// kernels over the same blocks.  Assembled once from the per-TU tables.
 struct KernelSet {
-  int B1, B2, SB, L;
-  KFn search, mark, blocks, states, finalize;
-  PFn prefix;
-  KFn fieldwalk;  // per-step field-walk search kernel with the same blocks (big geometry only)
-  KFn coarse;     // packed-int16 filter search kernel with the same blocks (big geometry only)
-  std::atomic<int> occ_c{-1};
-  std::atomic<int> occ_fw{-1};  // resident CTAs per SM for `fieldwalk` (lazy)
-  std::atomic<int> occ{-1};  // resident CTAs per SM for `search` (lazy; shared by all devices)
+  int B1 = 0, B2 = 0, SB = 0, L = 0;
+  KFn search = nullptr, mark = nullptr, blocks = nullptr, states = nullptr, finalize = nullptr;
+  PFn prefix = nullptr;
+  KFn fieldwalk = nullptr;  // per-step field-walk search kernel with the same blocks (big geometry only)
+  KFn coarse = nullptr;     // packed-int16 filter search kernel with the same blocks (big geometry only)
+  std::atomic<int> occ{-1};     // resident CTAs per SM for `search` (lazy; shared by all devices)
+  std::atomic<int> occ_fw{-1};  // ... for `fieldwalk`
+  std::atomic<int> occ_c{-1};   // ... for `coarse`
 };
 
-#define QB_KS(B1, B2, SB, L)                                                                             \
-  KernelSet {                                                                                            \
-    B1, B2, SB, L, table_kernel<B1, B2, SB, L, TPB>, collect_mark_kernel<B1, B2, SB, L>,                \
-        collect_blocks_kernel<B1, B2, SB, L>, collect_states_kernel<B1, B2, SB, L>,                      \
-        table_finalize_kernel<B1, B2, SB, L>, prefix_eval_kernel<B1, B2, SB, L>, nullptr, nullptr        \
-  }
-#define QB_KSC(B1, B2, L)                                                                                \
-  KernelSet {                                                                                            \
-    B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
-        collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
-        table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>, nullptr,                  \
-        coarse_kernel<B1, B2, QB_COARSE_B1, QB_COARSE_B2, L, TPB>                                        \
-  }
-#define QB_KSF(B1, B2, L)                                                                                \
-  KernelSet {                                                                                            \
-    B1, B2, 0, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                    \
-        collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
-        table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>,                           \
-        fieldwalk_kernel<L, TPB>, coarse_kernel<B1, B2, QB_COARSE_B1, QB_COARSE_B2, L, TPB>              \
-  }
-
-// Small problems (free bits < BIG_BE): one block of 2^L states per chunk, no sub-blocks.
-// Large problems: 2^10-entry table (BIG_BE = 10 block bits), L free bits per chunk.
-#ifndef QB_BIG_B1
-#define QB_BIG_B1 5
-#define QB_BIG_B2 5
-#endif
-#ifndef QB_BIG_SB
-#define QB_BIG_SB 0
-#endif
-#ifndef QB_COARSE_B1  // coarse pass split of the 10 table bits: u rows x w columns (measured best 4 x 6)
-#define QB_COARSE_B1 4
-#define QB_COARSE_B2 6
-#endif
-constexpr int BIG_B1 = QB_BIG_B1, BIG_B2 = QB_BIG_B2, BIG_SB = QB_BIG_SB, BIG_BE = BIG_B1 + BIG_B2 + BIG_SB;
-static KernelSet g_sets[] = {
-    QB_KS(0, 1, 0, 1),  QB_KS(1, 1, 0, 2),  QB_KS(1, 2, 0, 3),  QB_KS(2, 2, 0, 4),  QB_KS(2, 3, 0, 5),
-    QB_KS(3, 3, 0, 6),  QB_KS(3, 4, 0, 7),  QB_KS(4, 4, 0, 8),  QB_KS(4, 5, 0, 9),  QB_KSC(BIG_B1, BIG_B2, 10),
-#if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB != 10
-    QB_KS(BIG_B1, BIG_B2, BIG_SB, BIG_BE),
-#endif
-#if QB_BIG_SB == 0 && QB_BIG_B1 + QB_BIG_B2 == 10
-    QB_KSF(BIG_B1, BIG_B2, 11), QB_KSF(BIG_B1, BIG_B2, 12), QB_KSF(BIG_B1, BIG_B2, 13), QB_KSF(BIG_B1, BIG_B2, 14),
-    QB_KSF(BIG_B1, BIG_B2, 16), QB_KSF(BIG_B1, BIG_B2, 18),
-    QB_KSF(BIG_B1, BIG_B2, 20), QB_KSF(BIG_B1, BIG_B2, 22),
-#else
-#if QB_BIG_B1 + QB_BIG_B2 + QB_BIG_SB < 11
-    QB_KS(BIG_B1, BIG_B2, BIG_SB, 11),
-#endif
-    QB_KS(BIG_B1, BIG_B2, BIG_SB, 12), QB_KS(BIG_B1, BIG_B2, BIG_SB, 13),
-    QB_KS(BIG_B1, BIG_B2, BIG_SB, 14), QB_KS(BIG_B1, BIG_B2, BIG_SB, 16),
-    QB_KS(BIG_B1, BIG_B2, BIG_SB, 18), QB_KS(BIG_B1, BIG_B2, BIG_SB, 20), QB_KS(BIG_B1, BIG_B2, BIG_SB, 22),
-#endif
-};
+static std::vector<std::unique_ptr<KernelSet>>& kernel_sets() {
+  static std::vector<std::unique_ptr<KernelSet>> sets = [] {
+    std::vector<std::unique_ptr<KernelSet>> v;
+    int nt = 0, nc = 0, nf = 0;
+    const TableFns* t = table_fns(&nt);
+    const LFn* c = coarse_fns(&nc);
+    const LFn* f = fieldwalk_fns(&nf);
+    for (int i = 0; i < nt; ++i) {
+      auto k = std::make_unique<KernelSet>();
+      k->B1 = t[i].B1; k->B2 = t[i].B2; k->L = t[i].L;
+      k->search = t[i].search; k->mark = t[i].mark; k->blocks = t[i].blocks; k->states = t[i].states;
+      k->finalize = t[i].finalize; k->prefix = t[i].prefix;
+      if (k->B1 + k->B2 == BIG_BE) {
+        for (int j = 0; j < nc; ++j)
+          if (c[j].L == k->L) k->coarse = c[j].fn;
+        for (int j = 0; j < nf; ++j)
+          if (f[j].L == k->L) k->fieldwalk = f[j].fn;
+      }
+      v.push_back(std::move(k));
+    }
+    return v;
+  }();
+  return sets;
+}
 
 static KernelSet* find_set(int BE, int L) {
-  for (auto& s : g_sets)
-    if (s.B1 + s.B2 + s.SB == BE && s.L == L) return &s;
+  for (auto& s : kernel_sets())
+    if (s->B1 + s->B2 + s->SB == BE && s->L == L) return s.get();
   return nullptr;
 }
 
@@ -617,8 +580,8 @@ static int prefix_impl(const double* coeffs, int n, int k, uint64_t c_begin, uin
   if (k < 0 || k >= n) return fail(QB_E_ARG, "k out of range");
   const int L = n - k;
   KernelSet* ks = nullptr;
-  for (auto& s : g_sets)
-    if (s.L == L && (L <= BIG_BE ? s.B1 + s.B2 + s.SB == L : s.B1 == BIG_B1 && s.B2 == BIG_B2)) ks = &s;
+  for (auto& s : kernel_sets())
+    if (s->L == L && (L <= BIG_BE ? s->B1 + s->B2 + s->SB == L : s->B1 == BIG_B1 && s->B2 == BIG_B2)) ks = s.get();
   if (!ks) return fail(QB_E_ARG, "no traversal kernel with L = n - k = " + std::to_string(L));
   if (c_begin + count > (1ull << k) || count == 0) return fail(QB_E_ARG, "chunk range out of range");
   Device* dev = nullptr;
@@ -649,11 +612,6 @@ static int prefix_impl(const double* coeffs, int n, int k, uint64_t c_begin, uin
 }
 
 // ------------------------------------------------------------------ batch (config C)
-using BatchFn = void (*)(const BatchParams);
-static const BatchFn g_batch[] = {nullptr,
-                                  batch_kernel<0, 1>, batch_kernel<1, 1>, batch_kernel<1, 2>, batch_kernel<2, 2>,
-                                  batch_kernel<2, 3>, batch_kernel<3, 3>, batch_kernel<3, 4>, batch_kernel<4, 4>,
-                                  batch_kernel<4, 5>, batch_kernel<5, 5>};
 
 static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                       double* kernel_ms) {
@@ -680,7 +638,10 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
     threads = (threads + 31) / 32 * 32;
     BatchParams bp{dev->d_batch_coeffs, dev->d_batch_out, n, (int)count};
     QB_CUDA(cudaEventRecord(dev->ev0, st));
-    g_batch[B]<<<(unsigned)count, threads, 0, st>>>(bp);
+    int nb = 0;
+    const BatchFn* batch = batch_fns(&nb);
+    if (B >= nb || !batch[B]) return fail(QB_E_INTERNAL, "no batch kernel for B=" + std::to_string(B));
+    batch[B]<<<(unsigned)count, threads, 0, st>>>(bp);
     QB_CUDA(cudaGetLastError());
     QB_CUDA(cudaEventRecord(dev->ev1, st));
     std::vector<BatchOut> out(count);

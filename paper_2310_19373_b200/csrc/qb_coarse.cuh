@@ -17,9 +17,6 @@
 #pragma once
 #include "qb_table.cuh"
 
-#ifndef QB_PACKED_ROWS
-#define QB_PACKED_ROWS 1  // add A_u to both packed fields, extract once per block (CB = 2^13; measured 38.1 -> 37.1 ms)
-#endif
 
 namespace qb {
 

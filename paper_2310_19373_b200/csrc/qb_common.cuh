@@ -12,6 +12,14 @@
 #include <climits>
 #include <cstdint>
 
+// tunables shared by kernels and host planning (measured on B200)
+#ifndef QB_MINB
+#define QB_MINB 5  // resident CTAs per SM requested for the table kernel: 96 registers (20 warps/SM)
+#endif
+#ifndef QB_PACKED_ROWS
+#define QB_PACKED_ROWS 1  // coarse kernel: A_u added to both packed fields, one extraction per block
+#endif
+
 namespace qb {
 
 constexpr int NMAX = 40;   // reference core.py:24 MAX_DIM

@@ -25,9 +25,6 @@
 #ifndef QB_PREFIX_UNROLL
 #define QB_PREFIX_UNROLL 1  // unroll of the chunk-start evaluation loop over prefix bits
 #endif
-#ifndef QB_MINB
-#define QB_MINB 5  // resident CTAs per SM requested from ptxas: caps registers at 96 (20 warps/SM)
-#endif
 
 namespace qb {
 

@@ -1,14 +1,13 @@
 #!/bin/bash
-# Build experimental library variants into build/exp (each: tag + -D flags), in parallel.
+# Build experimental library variants into build/exp (stdin lines: "<tag> [-DFLAG=...]..."), one after
+# another (each build already compiles its translation units in parallel).
 cd "$(dirname "$0")/.."
 mkdir -p build/exp
-build_one() {
-  tag=$1; shift
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -shared \
-    "$@" -o build/exp/libqb_$tag.so paper_2310_19373_b200/csrc/qb_api.cu 2> build/exp/$tag.log && echo "built $tag"
-}
 while read -r tag flags; do
   [ -z "$tag" ] && continue
-  build_one $tag $flags &
+  python -c "
+import sys; sys.path.insert(0, '.')
+from paper_2310_19373_b200 import _lib
+_lib.build(output='build/exp/libqb_$tag.so', defines='$flags'.split())
+" > build/exp/$tag.log 2>&1 && echo "built $tag" || echo "FAILED $tag (build/exp/$tag.log)"
 done
-wait
