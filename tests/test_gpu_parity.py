@@ -385,3 +385,24 @@ def test_adversarial_value_ranges_coarse_kernel(kind):
             b = _lib.solve(inst.coeffs, *args, variant=_lib.VARIANT_COARSE)
             assert b.variant == _lib.VARIANT_COARSE
             assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (kind, seed, args)
+
+
+def test_concurrent_host_threads():
+    """ctypes releases the GIL: several host threads solving at once (as a thread pool over the
+    reference's entry points would) must each get their own correct answer."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cases = [instances.config_coeffs(name, rep, n=n) for name in ("D", "E") for rep in range(4) for n in (18, 26)]
+    want = [O.expected_argmin(c, 0)[0] if c.shape[0] <= 20 else None for c in cases]
+    serial = [int(_lib.solve(c).argmin_bits) for c in cases]
+
+    def job(i):
+        return int(qb.solve_incremental(qb.QuboInstance(cases[i])).minimizer.astype(np.uint64)
+                   .dot(np.uint64(1) << np.arange(cases[i].shape[0], dtype=np.uint64)))
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        got = list(pool.map(job, range(len(cases)) , chunksize=1))
+    assert got == serial
+    for g, w in zip(got, want):
+        if w is not None:
+            assert g == w
