@@ -406,3 +406,19 @@ def test_concurrent_host_threads():
     for g, w in zip(got, want):
         if w is not None:
             assert g == w
+
+
+@pytest.mark.parametrize("name", ["A", "B", "D"])
+def test_n40_other_instance_types(name):
+    """n=40 with the other BASELINE value distributions (int +-100, dense fp32 N(0,1), int +-1000):
+    the default coarse kernel and the fp32 table kernel agree, and the argmin is the exact minimum
+    of its own 2^23-state subspace (CPU oracle)."""
+    c = instances.config_coeffs(name, 0, n=40)
+    a = _lib.solve(c)
+    b = _lib.solve(c, variant=_lib.VARIANT_TABLE)
+    assert a.variant == _lib.VARIANT_COARSE and b.variant == _lib.VARIANT_TABLE
+    assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key)
+    x = int(a.argmin_bits)
+    m = 17
+    bits, val, _ = O.solve_subspaces(c, m, x >> (40 - m), (x >> (40 - m)) + 1)
+    assert bits == x and val == a.value
