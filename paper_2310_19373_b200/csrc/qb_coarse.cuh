@@ -26,9 +26,6 @@ namespace qb {
 // (LDCU.128 = 8 states, broadcast through the operand path, not replicated per lane), and
 // VIMNMX3.U16x2 folds two candidate pairs into the running pair-minimum (4 states per min).
 constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw and Tc components
-#ifndef QB_COARSE_ROLLED
-#define QB_COARSE_ROLLED 0  // 1: rolled row loop (measured slower: runtime table addresses become per-thread LDCs)
-#endif
 #ifndef QB_EXACT_NOINLINE
 #define QB_EXACT_NOINLINE 1  // long chunks call the exact re-evaluation out of line (measured n=40: 52 -> 41 ms)
 #endif
@@ -69,34 +66,7 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
 #pragma unroll
     for (int m = 0; m < (1 << (i - 1)); ++m) Bw2[m + (1 << (i - 1))] = Bw2[m] + d;
   }
-#if QB_COARSE_ROLLED
-  // rows in a rolled loop over row pairs (u0 = 2g, u0 + 1): the uniform table address depends on g,
-  // which bounds how far ptxas can hoist the LDCU.128 loads (unrolled, it exhausts the 63 uniform
-  // registers and spills); A_u from the bits of g with predicated adds
-  int rmin = INT_MAX;
-#pragma unroll 1
-  for (int g = 0; g < NU / 2; ++g) {
-    int Ag = -2 * CB;
-#pragma unroll
-    for (int i = 1; i < B1; ++i) Ag += ((g >> (i - 1)) & 1) ? hc[B2 + i] : 0;
-    const unsigned* trow = &p.Tc2[(2 * g) * NP];
-    int r[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      unsigned acc2 = 0u;
-#pragma unroll
-      for (int m = 0; m < NP; m += 4) {
-        const uint4 t = *reinterpret_cast<const uint4*>(trow + h * NP + m);
-        const unsigned c0 = Bw2[m] + t.x, c1 = Bw2[m + 1] + t.y;
-        const unsigned c2 = Bw2[m + 2] + t.z, c3 = Bw2[m + 3] + t.w;
-        acc2 = (m == 0) ? umin2(c0, c1) : umin3(acc2, c0, c1);
-        acc2 = umin3(acc2, c2, c3);
-      }
-      r[h] = (int)min(acc2 & 0xffffu, acc2 >> 16) + Ag + (h ? hc[B2] : 0);
-    }
-    rmin = min(min(rmin, r[0]), r[1]);
-  }
-#elif QB_PACKED_ROWS
+#if QB_PACKED_ROWS
   // A2[u] = (A_u + 2^14) in both fields; candidate fields (Bw + 2^13) + (Tc + 2^13) + (A + 2^14) stay in
   // [0, 2^16): rows are folded packed and unpacked once per block
   unsigned A2[NU];

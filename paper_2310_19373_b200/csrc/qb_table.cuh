@@ -97,27 +97,12 @@ __device__ __forceinline__ void subset_sums(float* S, float base, const float* h
 }
 
 // Minimum over the 2^(B+SB) states of a super-block, relative to its base value V (all block
-// bits zero).  The B table bits are split into u (B1 high) and w (B2 low); the SB sub-block
-// bits (positions B..B+SB-1) select one of P = 2^SB sub-blocks that share every table load:
-//     f(s, u, w) = V + delta_s + A^s_u + Bw^s_w + T(u, w)
-// with H^s = H + Q[.][sub bits of s], Bw^s = subset sums of H^s over w, A^s walked over u in
-// Gray order, delta_s = the sub-block bits' own value given the outer state (uses F).
-// Per state: half an FADD2 (two states, T pair from the constant bank through uniform
-// registers), half an FMNMX3, and 1/(2P) of an LDCU.128.
-#ifndef QB_TSMEM
-#define QB_TSMEM 0  // 1: stage T in shared memory and read it with broadcast LDS.128
-#endif
-
-
-__device__ __forceinline__ float4 t_lds128(unsigned addr) {
-  float4 v;
-  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
-}
-
+// bits zero).  The B table bits are split into u (B1 high) and w (B2 low):
+//     f(u, w) = V + A_u + Bw_w + T(u, w)
+// with A / Bw subset sums of the fields H.  Per state: half an FADD2 (two states, T pair from the
+// constant bank through uniform registers), half an FMNMX3, and a quarter of an LDCU.128.
 template <int B1, int B2, int SB, int NF>
-__device__ __forceinline__ float block_min_p1(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF],
-                                              unsigned tsm = 0) {
+__device__ __forceinline__ float block_min_p1(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
   constexpr int B = B1 + B2, NU = 1 << B1, NW = 1 << B2, P = 1 << SB;
   static_assert(B2 >= 1, "inner low part needs at least one bit");
   float rmin = 0.f;
@@ -155,22 +140,11 @@ __device__ __forceinline__ float block_min_p1(const TableParams& p, const float 
         if (kk + h >= NU) { ru[h] = ru[0]; continue; }
         const int u = kk + h;
         float acc = 0.f;
-        if constexpr (QB_TSMEM && NW >= 4) {
 #pragma unroll
-          for (int w = 0; w < NW; w += 4) {
-            const float4 t4 = t_lds128(tsm + 4u * (u * NW + w));
-            const float2 c0 = add_f32x2(make_float2(Bw[w], Bw[w + 1]), make_float2(t4.x, t4.y));
-            const float2 c1 = add_f32x2(make_float2(Bw[w + 2], Bw[w + 3]), make_float2(t4.z, t4.w));
-            acc = (w == 0) ? fminf(c0.x, c0.y) : fminf(fminf(acc, c0.x), c0.y);
-            acc = fminf(fminf(acc, c1.x), c1.y);
-          }
-        } else {
-#pragma unroll
-          for (int w = 0; w < NW; w += 2) {
-            const float2 t = *reinterpret_cast<const float2*>(&p.T[u * NW + w]);
-            const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
-            acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
-          }
+        for (int w = 0; w < NW; w += 2) {
+          const float2 t = *reinterpret_cast<const float2*>(&p.T[u * NW + w]);
+          const float2 c = add_f32x2(make_float2(Bw[w], Bw[w + 1]), t);
+          acc = (w == 0) ? fminf(c.x, c.y) : fminf(fminf(acc, c.x), c.y);
         }
         ru[h] = acc + A[u];
       }
@@ -180,82 +154,10 @@ __device__ __forceinline__ float block_min_p1(const TableParams& p, const float 
   return rmin;
 }
 
-// SB >= 1: P = 2^SB sub-blocks share every T load.  To keep registers low the u rows are
-// visited in Gray order and each sub-block's A_u is one running register (one FADD per
-// u-step), so only P x 2^B2 Bw values and P x B1 high fields stay live.
 template <int B1, int B2, int SB, int NF>
-__device__ __forceinline__ float block_min_shared(const TableParams& p, const float (&H)[B1 + B2],
-                                                  const float (&F)[NF]) {
-  constexpr int B = B1 + B2, NU = 1 << B1, NW = 1 << B2, P = 1 << SB;
-  static_assert(B2 >= 2 && (P % 2) == 0, "shared-table variant needs B2 >= 2 and an even sub-block count");
-  float Bw[P][NW];
-  float Hh[P][B1 > 0 ? B1 : 1];
-  float A[P];
-#pragma unroll
-  for (int s = 0; s < P; ++s) {
-    float hs[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-      float h = H[i];
-#pragma unroll
-      for (int t = 0; t < SB; ++t)
-        if ((s >> t) & 1) h += p.Qs[i][B + t];
-      hs[i] = h;
-    }
-    float dl = 0.f;
-#pragma unroll
-    for (int t = 0; t < SB; ++t) {
-      if (!((s >> t) & 1)) continue;
-      dl += p.d[B + t] + F[t];
-#pragma unroll
-      for (int t2 = t + 1; t2 < SB; ++t2)
-        if ((s >> t2) & 1) dl += p.Qs[B + t][B + t2];
-    }
-    Bw[s][0] = 0.f;
-#pragma unroll
-    for (int i = 0; i < B2; ++i)
-#pragma unroll
-      for (int w = 0; w < (1 << i); ++w) Bw[s][w + (1 << i)] = Bw[s][w] + hs[i];
-#pragma unroll
-    for (int i = 0; i < B1; ++i) Hh[s][i] = hs[B2 + i];
-    A[s] = dl;
-  }
-  float rmin = 0.f;
-#pragma unroll
-  for (int k = 0; k < NU; ++k) {
-    const int u = k ^ (k >> 1);
-    if (k > 0) {
-      const int i = ctz_c(k);
-      const bool up = (u >> i) & 1;
-#pragma unroll
-      for (int s = 0; s < P; ++s) A[s] = up ? (A[s] + Hh[s][i]) : (A[s] - Hh[s][i]);
-    }
-    float acc[P];
-#pragma unroll
-    for (int w = 0; w < NW; w += 4) {
-      const float4 t4 = *reinterpret_cast<const float4*>(&p.T[u * NW + w]);
-#pragma unroll
-      for (int s = 0; s < P; ++s) {
-        const float2 c0 = add_f32x2(make_float2(Bw[s][w], Bw[s][w + 1]), make_float2(t4.x, t4.y));
-        const float2 c1 = add_f32x2(make_float2(Bw[s][w + 2], Bw[s][w + 3]), make_float2(t4.z, t4.w));
-        acc[s] = (w == 0) ? fminf(c0.x, c0.y) : fminf(fminf(acc[s], c0.x), c0.y);
-        acc[s] = fminf(fminf(acc[s], c1.x), c1.y);
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < P; s += 2) {
-      const float r0 = acc[s] + A[s], r1 = acc[s + 1] + A[s + 1];
-      rmin = (k == 0 && s == 0) ? fminf(r0, r1) : fminf(fminf(rmin, r0), r1);
-    }
-  }
-  return rmin;
-}
-
-template <int B1, int B2, int SB, int NF>
-__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF],
-                                           unsigned tsm = 0) {
-  if constexpr (SB == 0) return block_min_p1<B1, B2, SB, NF>(p, H, F, tsm);
-  else return block_min_shared<B1, B2, SB, NF>(p, H, F);
+__device__ __forceinline__ float block_min(const TableParams& p, const float (&H)[B1 + B2], const float (&F)[NF]) {
+  static_assert(SB == 0, "sub-block table sharing was measured slower (register spills) and is not built");
+  return block_min_p1<B1, B2, SB, NF>(p, H, F);
 }
 
 // Every state of super-block j of chunk prefix s, evaluated directly from its base (finalize and
@@ -354,13 +256,6 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
   constexpr int LO = L - BE;
   constexpr int NF = (L - B) > 0 ? (L - B) : 1;
   static_assert(LO >= 0, "block bits exceed chunk bits");
-  unsigned tsm_base = 0;
-  if constexpr (QB_TSMEM) {
-    __shared__ __align__(16) float sT[1 << B];
-    for (int z = threadIdx.x; z < (1 << B); z += TPB) sT[z] = p.T[z];
-    __syncthreads();
-    tsm_base = (unsigned)__cvta_generic_to_shared(sT);
-  }
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
   const int lane = threadIdx.x & 31;
@@ -387,9 +282,7 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
         const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
         outer_flip<B, L, BE>(p, BE + r, sg, V, H, F);
       }
-      unsigned tsm = tsm_base;
-      if constexpr (QB_TSMEM) asm volatile("" : "+r"(tsm));  // no hoisting of table loads across blocks
-      const float rm = block_min<B1, B2, SB, NF>(p, H, F, tsm);
+      const float rm = block_min<B1, B2, SB, NF>(p, H, F);
       const long long val = V + (long long)rm;
       cmin = min(cmin, val);
       if (val <= best.val) {
