@@ -138,14 +138,20 @@ class ClockSampler:
 
 
 def dist_setup(gpus: int):
+    """One process per GPU (torchrun).  QB_DIST_BACKEND=gloo forces the CPU collective, which lets
+    several ranks share one GPU for a functional test of the N>1 path (their shard kernels are
+    independent; the only exchange is the host-side all-reduce)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    if torch.cuda.is_available():
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        import torch
         import torch.distributed as dist
 
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("QB_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
@@ -278,10 +284,12 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    coll_dev = "cuda" if world == 1 or torch.distributed.get_backend() == "nccl" else "cpu"
+
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
