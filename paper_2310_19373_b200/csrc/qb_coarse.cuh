@@ -31,15 +31,18 @@ constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw 
 #endif
 
 // exact fp32 re-evaluation of one block, out of line (rare path: keeps its 64 live table-loop
-// registers out of the coarse loop's allocation)
-template <int B1, int B2, int NF>
-__device__ __noinline__ float exact_block_min_ool(const TableParams& p, const float* Hp, const float* Fp) {
-  float H[B1 + B2], F[NF];
+// registers out of the coarse loop's allocation).  The fields travel by value: passing their
+// address would pin H in local memory and cost a store on every outer flip (measured 5 STL/block).
+template <int B>
+struct FieldVec {
+  float h[B];
+};
+template <int B1, int B2>
+__device__ __noinline__ float exact_block_min_ool(const TableParams& p, const FieldVec<B1 + B2> hv) {
+  float H[B1 + B2], F[1] = {0.f};  // block_min<.., SB = 0, ..> never reads the outer fields
 #pragma unroll
-  for (int i = 0; i < B1 + B2; ++i) H[i] = Hp[i];
-#pragma unroll
-  for (int i = 0; i < NF; ++i) F[i] = Fp[i];
-  return block_min<B1, B2, 0, NF>(p, H, F);
+  for (int i = 0; i < B1 + B2; ++i) H[i] = hv.h[i];
+  return block_min<B1, B2, 0, 1>(p, H, F);
 }
 
 __device__ __forceinline__ unsigned umin2(unsigned a, unsigned b) {
@@ -160,10 +163,11 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
     base_eval<B, L>(p, s << L, L, V, H, F);
     int dir;
     const unsigned long long key_hi = chunk_key(p, s, dir);
-    long long cmin = LLONG_MAX;
+    long long cmin = LLONG_MAX, skip_min = LLONG_MAX;  // skip_min: least coarse value of a pruned block
     // pruning threshold: the better of this thread's best and the device-wide best so far (any
     // block whose bound exceeds a value some state attains holds neither a minimiser nor a tie)
     long long thr = min(best.val, __ldcg(p.gbest));
+    long long lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;  // prune when the coarse value exceeds it
     for (unsigned int j = 0; j < (1u << LO); ++j) {
       if (j) {
         const int r = __ffs(j) - 1;
@@ -175,20 +179,28 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
       long long gb = LLONG_MAX;
       if constexpr (LO <= 6) gb = __ldcg(p.gbest);
       const long long cb = V + ((long long)coarse_block_min<CB1, CB2>(p, H) << p.coarse_shift);
-      thr = min(thr, gb);
+      if constexpr (LO <= 6) {
+        thr = min(thr, gb);
+        lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;
+      }
       long long val;
       if (coarse_exact) {
         val = cb;
       } else {
-        const long long lb = cb - slack;
-        if (lb > thr) {  // no state of this block can beat or tie the best value seen
-          cmin = min(cmin, lb);
+        if (cb > lim) {  // bound cb - slack > thr: no state of this block can beat or tie the best value seen
+          skip_min = min(skip_min, cb);
           continue;
         }
         // short chunks (<= 64 blocks) re-evaluate often enough that inlining wins; long chunks call
         // out of line so the coarse loop keeps the registers
-        if constexpr (QB_EXACT_NOINLINE && LO > 6) val = V + (long long)exact_block_min_ool<B1, B2, NF>(p, H, F);
-        else val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
+        if constexpr (QB_EXACT_NOINLINE && LO > 6) {
+          FieldVec<B> hv;
+#pragma unroll
+          for (int i = 0; i < B; ++i) hv.h[i] = H[i];
+          val = V + (long long)exact_block_min_ool<B1, B2>(p, hv);
+        } else {
+          val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
+        }
       }
       cmin = min(cmin, val);
       if (val <= best.val) {
@@ -196,10 +208,12 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
         if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
         if (val < thr) {
           thr = val;
+          lim = val + slack;
           atomicMin(p.gbest, val);
         }
       }
     }
+    if (skip_min != LLONG_MAX) cmin = min(cmin, skip_min - slack);  // pruned blocks contribute their bound
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
   const Rec r = cta_reduce<TPB>(best);

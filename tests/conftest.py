@@ -21,6 +21,12 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def bench_golden():
+    with open(os.path.join(ROOT, "tests", "golden", "reference_bench.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
 def cuda_available():
     import torch
 

@@ -4,6 +4,8 @@ argmin exact and value bit-identical (the value is eval_upper of the argmin).  T
 every entry point's rule, on tie-heavy instances.
 """
 
+import io
+
 import numpy as np
 import pytest
 
@@ -422,3 +424,17 @@ def test_n40_other_instance_types(name):
     m = 17
     bits, val, _ = O.solve_subspaces(c, m, x >> (40 - m), (x >> (40 - m)) + 1)
     assert bits == x and val == a.value
+
+
+def test_bench_records_match_reference_bench(bench_golden):
+    # the reference's own `qubrute bench` rows (seconds dropped): same instances, same values
+    from paper_2310_19373_b200 import benchrec
+
+    a = bench_golden["args"]
+    recs = benchrec.run_bench(int(a[2]), int(a[4]), reps=int(a[6]), modes=a[8], threads=int(a[10]))
+    assert [(r.n, r.mode, r.rep) for r in recs] == [(n, m, rep) for n, m, rep, _ in bench_golden["rows"]]
+    assert [r.value for r in recs] == [float(v) for *_, v in bench_golden["rows"]]
+    assert all(r.seconds > 0 for r in recs)
+    text = io.StringIO()
+    benchrec.write_csv(recs, stream=text)
+    assert benchrec.parse_csv(text.getvalue()) == recs
