@@ -4,7 +4,7 @@
 //   * planning: choose chunk geometry (k prefix bits, L free bits, B inner bits) and the
 //     integer scaling 2^e that makes every device add exact;
 //   * per-device state: stream, events, persistent workspace, a mutex serialising calls;
-//   * launching the traversal / finalize / collect kernels and combining their output
+//   * launching the traversal / collect kernels and combining their output
 //     into the reference's result contract (minimiser, eval_upper value, tie key).
 // The reference's equivalents are solver.py:118-229 (dispatch, subspace fan-out, reduce)
 // and _kernels.py:12-75 (the numba kernels).
@@ -48,10 +48,11 @@ static int fail(int code, const std::string& msg) {
 // kernels over the same blocks.  Assembled once from the per-TU tables.
 struct KernelSet {
   int B1 = 0, B2 = 0, SB = 0, L = 0;
-  KFn search = nullptr, mark = nullptr, blocks = nullptr, states = nullptr, finalize = nullptr;
+  KFn search = nullptr, mark = nullptr, blocks = nullptr, states = nullptr;
   PFn prefix = nullptr;
   KFn fieldwalk = nullptr;  // per-step field-walk search kernel with the same blocks (big geometry only)
   KFn coarse = nullptr;     // packed-int16 filter search kernel with the same blocks (big geometry only)
+  KFn coarse_fin = nullptr; // its one-CTA record reduction (the coarse kernel only writes records)
   std::atomic<int> occ{-1};     // resident CTAs per SM for `search` (lazy; shared by all devices)
   std::atomic<int> occ_fw{-1};  // ... for `fieldwalk`
   std::atomic<int> occ_c{-1};   // ... for `coarse`
@@ -68,10 +69,13 @@ static std::vector<std::unique_ptr<KernelSet>>& kernel_sets() {
       auto k = std::make_unique<KernelSet>();
       k->B1 = t[i].B1; k->B2 = t[i].B2; k->L = t[i].L;
       k->search = t[i].search; k->mark = t[i].mark; k->blocks = t[i].blocks; k->states = t[i].states;
-      k->finalize = t[i].finalize; k->prefix = t[i].prefix;
+      k->prefix = t[i].prefix;
       if (k->B1 + k->B2 == BIG_BE) {
         for (int j = 0; j < nc; ++j)
-          if (c[j].L == k->L) k->coarse = c[j].fn;
+          if (c[j].L == k->L) {
+            k->coarse = c[j].fn;
+            k->coarse_fin = c[j].fin;
+          }
         for (int j = 0; j < nf; ++j)
           if (f[j].L == k->L) k->fieldwalk = f[j].fn;
       }
@@ -89,6 +93,9 @@ static KernelSet* find_set(int BE, int L) {
 }
 
 // ------------------------------------------------------------------ per-device state
+// candidates read back together with the collect counts (one host round trip when they fit)
+constexpr int kCandPre = 1024;
+
 struct Device {
   int id = -1;
   int sms = 0;
@@ -102,9 +109,12 @@ struct Device {
   size_t chunk_min_cap = 0;
   unsigned long long* d_cand = nullptr;
   size_t cand_cap = 0;
-  unsigned long long* d_work = nullptr;  // [0] chunk counter, [1] device-wide best (coarse kernel)
-  unsigned long long* d_counts = nullptr;  // [0] chunks, [1] blocks, [2] candidates
-  unsigned long long* h_counts = nullptr;  // pinned
+  // [0] chunk counter, [1] device-wide best (gbest_enc), [2] CTAs done, [3..5] collect counts
+  // (chunks, blocks, candidates): one zero memset before each search
+  unsigned long long* d_work = nullptr;
+  unsigned long long* d_counts = nullptr;  // = d_work + 3
+  // pinned readback, one copy per solve: [0..2] collect counts, then up to kCandPre candidates
+  unsigned long long* h_counts = nullptr;
   unsigned long long* d_lists = nullptr;   // chunk list | block list
   size_t list_cap = 0;
   double* d_coeffs = nullptr;              // fp64 coefficients for the overflow reduction
@@ -137,9 +147,9 @@ static int get_device(Device** out) {
     QB_CUDA(cudaEventCreate(&d->evs));
     QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
     QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
-    QB_CUDA(cudaMalloc(&d->d_work, 2 * sizeof(unsigned long long)));
-    QB_CUDA(cudaMalloc(&d->d_counts, 3 * sizeof(unsigned long long)));
-    QB_CUDA(cudaMallocHost(&d->h_counts, 3 * sizeof(unsigned long long)));
+    QB_CUDA(cudaMalloc(&d->d_work, 6 * sizeof(unsigned long long)));
+    d->d_counts = d->d_work + 3;
+    QB_CUDA(cudaMallocHost(&d->h_counts, (3 + kCandPre) * sizeof(unsigned long long)));
     QB_CUDA(cudaMalloc(&d->d_red, 2 * sizeof(unsigned long long)));
     QB_CUDA(cudaMallocHost(&d->h_red, 2 * sizeof(unsigned long long)));
     g_devs[dev] = std::move(d);
@@ -209,9 +219,15 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     e = (int)std::floor(std::log2(LIM / M));
   }
   std::vector<double> q((size_t)n * n);
+  // x * 2^e is the correctly rounded x.2^e, i.e. ldexp(x, e), whenever 2^e itself is a normal double
+  auto scaled = [&](double x, int ee) { return (ee >= -960 && ee <= 960) ? x * std::ldexp(1.0, ee) : std::ldexp(x, ee); };
   for (int guard = 0; guard < 8; ++guard, --e) {
+    const double sc = std::ldexp(1.0, e);
+    const bool mul = e >= -960 && e <= 960;
     for (int i = 0; i < n; ++i)
-      for (int j = 0; j < n; ++j) q[(size_t)i * n + j] = (j >= i) ? std::nearbyint(std::ldexp(c[(size_t)i * n + j], e)) : 0.0;
+      for (int j = 0; j < n; ++j)
+        q[(size_t)i * n + j] =
+            (j >= i) ? std::nearbyint(mul ? c[(size_t)i * n + j] * sc : std::ldexp(c[(size_t)i * n + j], e)) : 0.0;
     auto getq = [&](int i, int j) { return i < j ? q[(size_t)i * n + j] : q[(size_t)j * n + i]; };
     if (bound(getq) <= LIM) break;
     if (guard == 7) return fail(QB_E_INTERNAL, "quantization failed to meet the fp32 exactness bound");
@@ -219,7 +235,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
   bool exact = true;
   for (int i = 0; i < n && exact; ++i)
     for (int j = i; j < n; ++j)
-      if (std::ldexp(c[(size_t)i * n + j], e) != q[(size_t)i * n + j]) { exact = false; break; }
+      if (scaled(c[(size_t)i * n + j], e) != q[(size_t)i * n + j]) { exact = false; break; }
   pl.e = e;
   pl.exact = exact;
   pl.Eq = exact ? 0 : (nnz + 1) / 2 + 1;
@@ -232,16 +248,18 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     P.d[i] = (float)q[(size_t)i * n + i];
     for (int j = i + 1; j < n; ++j) P.Qs[i][j] = P.Qs[j][i] = (float)q[(size_t)i * n + j];
   }
-  // T by doubling: T[z + 2^b] = T[z] + q_bb + sum_{i<b} z_i q_ib  (exact integers, |T| < 2^24)
+  // T by doubling: T[z + 2^b] = T[z] + q_bb + R_b(z), R_b(z) = sum_{i<b} z_i q_ib itself built by
+  // doubling (R_b(z + 2^i) = R_b(z) + q_ib): 2^B exact integer additions in fp64, |T| < 2^24
   P.T[0] = 0.f;
+  double R[1 << (BMAX - 1)];
   for (int b = 0; b < B; ++b) {
     const double qbb = q[(size_t)b * n + b];
-    for (int z = 0; z < (1 << b); ++z) {
-      double t = (double)P.T[z] + qbb;
-      for (int i = 0; i < b; ++i)
-        if ((z >> i) & 1) t += q[(size_t)i * n + b];
-      P.T[z + (1 << b)] = (float)t;
+    R[0] = 0.0;
+    for (int i = 0; i < b; ++i) {
+      const double qib = q[(size_t)i * n + b];
+      for (int z = 0; z < (1 << i); ++z) R[z + (1 << i)] = R[z] + qib;
     }
+    for (int z = 0; z < (1 << b); ++z) P.T[z + (1 << b)] = (float)((double)P.T[z] + qbb + R[z]);
   }
   for (int z = (1 << B); z < (1 << BMAX); ++z) P.T[z] = 0.f;
   // coarse image for the filter kernel (qb_coarse.cuh): coarse unit 2^s quantized units, s the smallest
@@ -260,9 +278,10 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
   P.coarse_shift = cs;
   P.coarse_scale = (float)std::ldexp(1.0, -cs);
   const int bias = (int)field_max + 1;
+  const double cscale = std::ldexp(1.0, -cs);  // exact power of two: x * cscale == ldexp(x, -cs)
   for (int z = 0; z < (1 << BMAX); z += 2) {
-    const int t0 = (z < (1 << B)) ? (int)std::nearbyint(std::ldexp((double)P.T[z], -cs)) : 0;
-    const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint(std::ldexp((double)P.T[z + 1], -cs)) : 0;
+    const int t0 = (z < (1 << B)) ? (int)std::nearbyint((double)P.T[z] * cscale) : 0;
+    const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint((double)P.T[z + 1] * cscale) : 0;
     P.Tc2[z / 2] = (unsigned)(t0 + bias) | ((unsigned)(t1 + bias) << 16);
   }
   return QB_OK;
@@ -329,6 +348,13 @@ static double eval_bits(const double* c, int n, unsigned long long x) {
 }
 
 // ------------------------------------------------------------------ the solve
+#ifdef QB_HOST_TIMING
+#define QB_TMARK(tag)                                                                                  \
+  fprintf(stderr, "qbt %s %.2f\n", tag,                                                                \
+          std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count())
+#else
+#define QB_TMARK(tag) ((void)0)
+#endif
 static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long suffix, int m_tie, int rule,
                       uint32_t shard, uint32_t shard_count, int variant, qb_result* out,
                       std::vector<unsigned long long>* all_out = nullptr) {
@@ -349,6 +375,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
   std::lock_guard<std::mutex> guard(dev->mu);
+  QB_TMARK("device");
 
   Plan pl;
   pl.n = n;
@@ -370,7 +397,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
       std::ldexp(1.0, n - m_fix - BE) / (double)shard_count / ((double)dev->sms * QB_MINB * TPB);
   const bool coarse = pl.ks->coarse != nullptr &&
                       (variant == QB_VARIANT_COARSE || (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
+  QB_TMARK("geometry");
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl)) return rc;
+  QB_TMARK("quantize");
 
   TableParams& P = *pl.P;
   P.n = n;
@@ -418,7 +447,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   P.cta_out = dev->d_cta;
   P.final_out = dev->d_final;
   P.work = dev->d_work;
-  P.gbest = reinterpret_cast<long long*>(dev->d_work + 1);
+  P.gbest = dev->d_work + 1;
+  P.done = dev->d_work + 2;
   P.nrec = grid;
   const bool collect = !pl.exact || all_out != nullptr;
   P.mode = collect ? MODE_SEARCH_RECORD : MODE_SEARCH;
@@ -438,26 +468,60 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
 
   cudaStream_t st = dev->stream;
-  QB_CUDA(cudaMemsetAsync(dev->d_work, 0, sizeof(unsigned long long), st));
-  QB_CUDA(cudaMemsetAsync(dev->d_work + 1, 0x7f, sizeof(unsigned long long), st));  // "+infinity"
+  // chunk counter, device-wide best (+infinity), done counter and collect counts in one memset
+  QB_CUDA(cudaMemsetAsync(dev->d_work, 0, 6 * sizeof(unsigned long long), st));
+  QB_TMARK("memsets");
   QB_CUDA(cudaEventRecord(dev->ev0, st));
-  search_fn<<<grid, TPB, 0, st>>>(P);
+  search_fn<<<grid, TPB, 0, st>>>(P);  // table / field walk: the last CTA reduces the records into d_final
   QB_CUDA(cudaGetLastError());
+  out->launches = 1;
+  if (search_fn == ks.coarse) {
+    ks.coarse_fin<<<1, TPB, 0, st>>>(P);
+    QB_CUDA(cudaGetLastError());
+    out->launches = 2;
+  }
+  QB_TMARK("search_launched");
   QB_CUDA(cudaEventRecord(dev->evs, st));
-  ks.finalize<<<1, 1024, 0, st>>>(P);
-  QB_CUDA(cudaGetLastError());
+  out->param_bytes = sizeof(TableParams);
+
+  const int grid_mark = std::max(1, std::min((int)((nchunks + 255) / 256), dev->sms * 8));
+  // certified collect pass (collect path): every state within 2*Eq of the quantized minimum is listed
+  // for exact re-evaluation; the threshold is read on the device from the search's result
+  auto enqueue_collect = [&]() -> int {
+    ks.mark<<<grid_mark, 256, 0, st>>>(P);
+    QB_CUDA(cudaGetLastError());
+    ks.blocks<<<dev->sms * 4, 128, 0, st>>>(P);
+    QB_CUDA(cudaGetLastError());
+    ks.states<<<dev->sms * 2, 128, 0, st>>>(P);
+    QB_CUDA(cudaGetLastError());
+    out->launches += 3;
+    return QB_OK;
+  };
+  if (collect) {
+    P.mode = MODE_COLLECT;
+    P.theta_add = 2 * pl.Eq;
+    if (int rc = enqueue_collect()) return rc;
+  }
   QB_CUDA(cudaEventRecord(dev->ev1, st));
+  // one readback: the search result, and on the collect path the counts plus the first candidates
   QB_CUDA(cudaMemcpyAsync(dev->h_final, dev->d_final, sizeof(FinalOut), cudaMemcpyDeviceToHost, st));
+  if (collect) {
+    QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaMemcpyAsync(dev->h_counts + 3, dev->d_cand,
+                            std::min<size_t>(kCandPre, dev->cand_cap) * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));  // candidates beyond this are fetched below
+  }
+  QB_TMARK("enqueued");
   QB_CUDA(cudaStreamSynchronize(st));
+  QB_TMARK("synced");
   float ms = 0.f;
   QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
   out->kernel_ms = ms;
   QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->evs));
   out->search_ms = ms;
-  out->launches = 2;
-  out->param_bytes = sizeof(TableParams);
+  out->collect_ms = collect ? out->kernel_ms - out->search_ms : 0.0;
   const FinalOut fo = *dev->h_final;
-  if (!fo.found) return fail(QB_E_INTERNAL, "finalize found no state attaining the block minimum");
+  if (!fo.found) return fail(QB_E_INTERNAL, "search found no state attaining the block minimum");
 
   if (!collect) {
     out->argmin_bits = fo.x;
@@ -467,43 +531,25 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     if (host_tie_key(fo.x, n, m_tie, rule) != fo.key)
       return fail(QB_E_INTERNAL, "device tie key disagrees with the host tie key");
   } else {
-    // certified filter: every state within 2*Eq of the quantized minimum is re-evaluated exactly
-    P.mode = MODE_COLLECT;
-    P.theta = fo.val + 2 * pl.Eq;
-    const int grid_mark = std::max(1, std::min((int)((nchunks + 255) / 256), dev->sms * 8));
-    auto run_collect = [&]() -> int {
-      QB_CUDA(cudaMemsetAsync(dev->d_counts, 0, 3 * sizeof(unsigned long long), st));
-      ks.mark<<<grid_mark, 256, 0, st>>>(P);
-      QB_CUDA(cudaGetLastError());
-      ks.blocks<<<dev->sms * 4, 128, 0, st>>>(P);
-      QB_CUDA(cudaGetLastError());
-      ks.states<<<dev->sms * 2, 128, 0, st>>>(P);
-      QB_CUDA(cudaGetLastError());
-      out->launches += 3;
-      QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                              st));
-      QB_CUDA(cudaStreamSynchronize(st));
-      return QB_OK;
-    };
-    QB_CUDA(cudaEventRecord(dev->ev0, st));
-    if (int rc = run_collect()) return rc;
-    QB_CUDA(cudaEventRecord(dev->ev1, st));
-    QB_CUDA(cudaEventSynchronize(dev->ev1));
-    QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
-    out->kernel_ms += ms;
-    out->collect_ms = ms;
     if (dev->h_counts[0] > P.list_cap || dev->h_counts[1] > P.list_cap)
       return fail(QB_E_INTERNAL, "collect pass: more than " + std::to_string(P.list_cap) +
                                      " chunks or blocks within the certified bound");
     unsigned long long cnt = dev->h_counts[2];
     if (cnt == 0) return fail(QB_E_INTERNAL, "collect pass found no candidate");
+    const size_t prefetched = std::min<size_t>(kCandPre, dev->cand_cap);  // read back with the counts
+    bool recollected = false;
     if (cnt > P.cand_cap && all_out != nullptr && cnt <= (1ull << 27)) {
       // all-minimisers request with more ties than the buffer holds: grow it and collect again
       if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)cnt)) return rc;
       P.cand = dev->d_cand;
       P.cand_cap = dev->cand_cap;
-      if (int rc = run_collect()) return rc;
+      QB_CUDA(cudaMemsetAsync(dev->d_counts, 0, 3 * sizeof(unsigned long long), st));
+      if (int rc = enqueue_collect()) return rc;
+      QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              st));
+      QB_CUDA(cudaStreamSynchronize(st));
       cnt = dev->h_counts[2];
+      recollected = true;
     }
     if (cnt > P.cand_cap) {
       if (all_out != nullptr)
@@ -540,8 +586,12 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
       return QB_OK;
     }
     std::vector<unsigned long long> cand(cnt);
-    QB_CUDA(cudaMemcpyAsync(cand.data(), dev->d_cand, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    QB_CUDA(cudaStreamSynchronize(st));
+    if (!recollected && cnt <= prefetched) {
+      std::memcpy(cand.data(), dev->h_counts + 3, cnt * sizeof(unsigned long long));
+    } else {
+      QB_CUDA(cudaMemcpyAsync(cand.data(), dev->d_cand, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      QB_CUDA(cudaStreamSynchronize(st));
+    }
     double bv = 0.0;
     unsigned long long bx = 0, bk = ~0ull;
     bool have = false;
@@ -568,6 +618,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     out->value = bv;
     out->value_key = pl.exact ? ((unsigned long long)fo.val ^ (1ull << 63)) : ordered_double(bv);
   }
+  QB_TMARK("done");
   out->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return QB_OK;
 }
@@ -721,7 +772,6 @@ void qb_shutdown(void) {
     cudaFree(d->d_chunk_min);
     cudaFree(d->d_cand);
     cudaFree(d->d_work);
-    cudaFree(d->d_counts);
     cudaFreeHost(d->h_counts);
     cudaFree(d->d_lists);
     cudaFree(d->d_coeffs);

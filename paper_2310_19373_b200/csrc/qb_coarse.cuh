@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
     long long cmin = LLONG_MAX, skip_min = LLONG_MAX;  // skip_min: least coarse value of a pruned block
     // pruning threshold: the better of this thread's best and the device-wide best so far (any
     // block whose bound exceeds a value some state attains holds neither a minimiser nor a tie)
-    long long thr = min(best.val, __ldcg(p.gbest));
+    long long thr = min(best.val, gbest_dec(__ldcg(p.gbest)));
     long long lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;  // prune when the coarse value exceeds it
     for (unsigned int j = 0; j < (1u << LO); ++j) {
       if (j) {
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
       // device-wide best: short chunks (<= 64 blocks) refresh it every block, long chunks only at
       // the chunk start (measured: the per-block load costs ~5% at 1024 blocks per chunk)
       long long gb = LLONG_MAX;
-      if constexpr (LO <= 6) gb = __ldcg(p.gbest);
+      if constexpr (LO <= 6) gb = gbest_dec(__ldcg(p.gbest));
       const long long cb = V + ((long long)coarse_block_min<CB1, CB2>(p, H) << p.coarse_shift);
       if constexpr (LO <= 6) {
         thr = min(thr, gb);
@@ -209,13 +209,14 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
         if (val < thr) {
           thr = val;
           lim = val + slack;
-          atomicMin(p.gbest, val);
+          atomicMax(p.gbest, gbest_enc(val));
         }
       }
     }
     if (skip_min != LLONG_MAX) cmin = min(cmin, skip_min - slack);  // pruned blocks contribute their bound
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
+  // records only: the reduction runs as finalize_kernel (see there for why not in this tail)
   const Rec r = cta_reduce<TPB>(best);
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
 }

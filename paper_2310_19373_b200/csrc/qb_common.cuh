@@ -58,7 +58,7 @@ struct alignas(16) TableParams {
   unsigned long long suffix;       // value of the m_fix fixed high bits
   unsigned long long chunk_begin;  // chunk range [begin, end) scanned by this launch
   unsigned long long chunk_end;
-  long long theta;                 // collect threshold (mode 1)
+  long long theta_add;             // collect threshold = final_out->val + theta_add (2 Eq)
   long long* chunk_min;            // per-chunk minimum, indexed c - chunk_begin (approximate path)
   unsigned long long* cand;        // candidate states (mode 1)
   unsigned long long* cand_count;
@@ -66,7 +66,8 @@ struct alignas(16) TableParams {
   Rec* cta_out;                    // one record per CTA
   FinalOut* final_out;
   unsigned long long* work;        // dynamic chunk counter (zeroed before each search launch)
-  long long* gbest;                // device-wide best value so far (coarse kernel pruning threshold)
+  unsigned long long* gbest;       // device-wide best value so far, gbest_enc() form (0 = +infinity)
+  unsigned long long* done;        // CTAs finished (the last one reduces the records), zeroed per launch
   unsigned long long* counts;      // collect pass counters: [0] chunks, [1] blocks, [2] unused
   unsigned long long* chunk_list;  // chunk offsets (c - chunk_begin) whose minimum is <= theta
   unsigned long long* block_list;  // (chunk offset << 32) | block j, block minimum <= theta
@@ -76,6 +77,21 @@ struct alignas(16) TableParams {
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };
+
+// Device-wide best value as an order-inverting unsigned code: a larger code is a smaller value and
+// code 0 means "+infinity", so one zero memset initialises it with the counters beside it.
+__device__ __forceinline__ unsigned long long gbest_enc(long long v) {
+  return ~((unsigned long long)v ^ (1ull << 63));
+}
+__device__ __forceinline__ long long gbest_dec(unsigned long long e) {
+  return (long long)(~e ^ (1ull << 63));
+}
+
+// Collect threshold: the search's quantized minimum (written by its last CTA) plus the certified
+// margin; read from the device so the collect pass is enqueued without a host round trip.
+__device__ __forceinline__ long long collect_theta(const TableParams& p) {
+  return __ldcg(&p.final_out->val) + p.theta_add;
+}
 enum { MODE_SEARCH = 0, MODE_SEARCH_RECORD = 1, MODE_COLLECT = 2, MODE_REDUCE_VALUE = 3, MODE_REDUCE_KEY = 4 };
 
 

@@ -129,8 +129,7 @@ __global__ void __launch_bounds__(TPB, QB_MINB) fieldwalk_kernel(const __grid_co
     }
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
-  const Rec r = cta_reduce<TPB>(best);
-  if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
+  search_epilogue<FW_RB, L, TPB>(p, best);
 }
 
 }  // namespace qb

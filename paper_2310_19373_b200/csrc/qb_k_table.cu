@@ -1,4 +1,4 @@
-// Instantiations of the table-kernel family (search, collect stages, finalize, prefix hook).
+// Instantiations of the table-kernel family (search, collect stages, prefix hook).
 #include "qb_registry.h"
 #include "qb_table.cuh"
 
@@ -8,7 +8,7 @@ namespace qb {
   TableFns {                                                                                             \
     B1, B2, L, table_kernel<B1, B2, 0, L, TPB>, collect_mark_kernel<B1, B2, 0, L>,                       \
         collect_blocks_kernel<B1, B2, 0, L>, collect_states_kernel<B1, B2, 0, L>,                        \
-        table_finalize_kernel<B1, B2, 0, L>, prefix_eval_kernel<B1, B2, 0, L>                            \
+        prefix_eval_kernel<B1, B2, 0, L>                                                                 \
   }
 
 // small problems: one block of 2^L states per chunk (L = block bits <= 10); large problems: 10-bit

@@ -32,13 +32,14 @@ using BatchFn = void (*)(const BatchParams);
 // table-kernel family for one block shape (B1, B2) and chunk length L
 struct TableFns {
   int B1, B2, L;
-  KFn search, mark, blocks, states, finalize;
+  KFn search, mark, blocks, states;
   PFn prefix;
 };
 // a search kernel over the large-block (BIG_BE) geometry with chunk length L
 struct LFn {
   int L;
   KFn fn;
+  KFn fin;  // one-CTA record reduction for kernels that do not reduce in their own tail (or null)
 };
 
 const TableFns* table_fns(int* count);    // qb_k_table.cu

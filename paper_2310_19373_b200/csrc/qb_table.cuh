@@ -182,14 +182,100 @@ __device__ __forceinline__ void for_block_states(const TableParams& p, unsigned 
   }
 }
 
+// End of every search kernel (table, coarse, field walk): publish this CTA's record; the last CTA
+// to finish reduces all records and writes p.final_out (the former separate finalize launch).
+// Exact search (MODE_SEARCH): it also re-evaluates the winning block with all its threads and
+// picks the lowest-key minimiser inside it.  Recording search (MODE_SEARCH_RECORD, the certified
+// collect path): only the minimum value is needed (the collect pass reads it as its threshold).
+template <int B, int L, int TPB>
+__device__ __noinline__ void search_final(const TableParams& p);
+
+template <int B, int L, int TPB>
+__device__ __noinline__ void search_tail(const TableParams& p, const Rec r) {
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    p.cta_out[blockIdx.x] = r;
+    __threadfence();  // the record is visible device-wide before the count that announces it
+    last = atomicAdd(p.done, 1ull) == (unsigned long long)gridDim.x - 1ull;
+  }
+  __syncthreads();
+  if (last) search_final<B, L, TPB>(p);
+}
+
+template <int B, int L, int TPB>
+__device__ __forceinline__ void search_epilogue(const TableParams& p, const Rec& mine) {
+  search_tail<B, L, TPB>(p, cta_reduce<TPB>(mine));
+}
+
+// The last CTA's work: reduce every CTA record, then (exact search) rescan the winning block.
+template <int B, int L, int TPB>
+__device__ __noinline__ void search_final(const TableParams& p) {
+  __threadfence();
+  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  for (int i = threadIdx.x; i < p.nrec; i += TPB) {
+    Rec o;
+    o.val = __ldcg(&p.cta_out[i].val);
+    o.K = __ldcg(&p.cta_out[i].K);
+    o.c = __ldcg(&p.cta_out[i].c);
+    o.j = __ldcg(&p.cta_out[i].j);
+    o.pad = 0u;
+    if (rec_less(o, best)) best = o;
+  }
+  best = cta_reduce<TPB>(best);
+  __shared__ Rec win;
+  if (threadIdx.x == 0) win = best;
+  __syncthreads();
+  best = win;
+  if (best.val == LLONG_MAX || p.mode != MODE_SEARCH) {
+    if (threadIdx.x == 0)
+      *p.final_out = FinalOut{best.val, ~0ull, 0ull, best.c, best.j, best.val != LLONG_MAX ? 1 : 0};
+    return;
+  }
+  const unsigned long long s = chunk_prefix(p, best.c);
+  int dir;
+  (void)chunk_key(p, s, dir);
+  const unsigned long long xo = (s << L) | ((unsigned long long)(best.j ^ (best.j >> 1)) << B);
+  unsigned int bk = ~0u, bz = 0u;
+  const unsigned int jj = best.j;
+  const long long target = best.val;
+  for_block_states<B, 0, L>(p, xo, threadIdx.x, TPB, [&](unsigned int zb, long long val) {
+    if (val == target) {
+      const unsigned int kin = inner_key(p, dir, jj, zb, B);
+      if (kin < bk) { bk = kin; bz = zb; }
+    }
+  });
+  // (key, state) minimum over the CTA; keys are unique within the block, so the state follows its key
+  const unsigned long long kz = ((unsigned long long)bk << 32) | bz;
+  unsigned long long m = kz;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, off));
+  __shared__ unsigned long long wmin[TPB / 32];
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < TPB / 32; ++w) m = min(m, wmin[w]);
+    const unsigned int k = (unsigned int)(m >> 32), z = (unsigned int)(m & 0xffffffffu);
+    *p.final_out = FinalOut{best.val, (best.K << B) | k, xo | z, best.c, best.j, k != ~0u ? 1 : 0};
+  }
+}
+
+// The same reduction as a one-CTA launch after a search kernel that only writes its records (the
+// coarse kernel: any code in its tail, even an out-of-line call, changes ptxas's integer-add pipe
+// split in the hot loop -- IADD3 on the ALU pipe vs VIADD on the FMA pipe -- measured 36 -> 39 ms).
+template <int B, int L, int TPB>
+__global__ void __launch_bounds__(TPB) finalize_kernel(const __grid_constant__ TableParams p) {
+  search_final<B, L, TPB>(p);
+}
+
 // ---- certified-filter collect pass (float path / all-minimisers), three small launches:
 // 1. chunks whose recorded minimum is <= theta -> chunk_list
 template <int B1, int B2, int SB, int L>
 __global__ void __launch_bounds__(256) collect_mark_kernel(const __grid_constant__ TableParams p) {
   const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+  const long long theta = collect_theta(p);
   for (unsigned long long ci = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; ci < nchunks;
        ci += (unsigned long long)gridDim.x * blockDim.x) {
-    if (p.chunk_min[ci] <= p.theta) {
+    if (p.chunk_min[ci] <= theta) {
       const unsigned long long idx = atomicAdd(&p.counts[0], 1ull);
       if (idx < p.list_cap) p.chunk_list[idx] = ci;
     }
@@ -203,6 +289,7 @@ __global__ void __launch_bounds__(128) collect_blocks_kernel(const __grid_consta
   constexpr int B = B1 + B2, BE = B + SB, LO = L - BE;
   constexpr int NF = (L - B) > 0 ? (L - B) : 1;
   const unsigned long long nlisted = min(p.counts[0], p.list_cap);
+  const long long theta = collect_theta(p);
   const unsigned long long total = nlisted << LO;
   for (unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (unsigned long long)gridDim.x * blockDim.x) {
@@ -213,7 +300,7 @@ __global__ void __launch_bounds__(128) collect_blocks_kernel(const __grid_consta
     long long V;
     float H[B], F[NF];
     base_eval<B, L>(p, xo, B, V, H, F);
-    if (V + (long long)block_min<B1, B2, SB, NF>(p, H, F) <= p.theta) {
+    if (V + (long long)block_min<B1, B2, SB, NF>(p, H, F) <= theta) {
       const unsigned long long idx = atomicAdd(&p.counts[1], 1ull);
       if (idx < p.list_cap) p.block_list[idx] = (ci << 32) | j;
     }
@@ -225,6 +312,7 @@ template <int B1, int B2, int SB, int L>
 __global__ void __launch_bounds__(128) collect_states_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2, BE = B + SB;
   const unsigned long long nblocks = min(p.counts[1], p.list_cap);
+  const long long theta = collect_theta(p);
   const int lane = threadIdx.x & 31;
   for (unsigned long long w = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nblocks;
        w += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
@@ -234,7 +322,7 @@ __global__ void __launch_bounds__(128) collect_states_kernel(const __grid_consta
     const unsigned long long s = chunk_prefix(p, p.chunk_begin + ci);
     const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
     for_block_states<B, SB, L>(p, xo, lane, 32, [&](unsigned int zb, long long val) {
-      if (val > p.theta) return;
+      if (val > theta) return;
       const unsigned long long x = xo | zb;
       if (p.mode == MODE_COLLECT) {
         const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
@@ -292,8 +380,7 @@ __global__ void __launch_bounds__(TPB, QB_MINB) table_kernel(const __grid_consta
     }
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
-  const Rec r = cta_reduce<TPB>(best);
-  if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
+  search_epilogue<B1 + B2, L, TPB>(p, best);
 }
 
 // Standalone chunk-start ("prefix") evaluation for the qb_prefix_eval test hook: runs the very
@@ -314,51 +401,6 @@ __global__ void prefix_eval_kernel(const __grid_constant__ TableParams p, double
   for (int i = 0; i < B; ++i) fields[idx * L + i] = ldexp((double)(H[i] + p.d[i]), -e);
 #pragma unroll
   for (int m = 0; m < L - B; ++m) fields[idx * L + B + m] = ldexp((double)(F[m] + p.d[B + m]), -e);
-}
-
-// Single CTA: reduce the per-CTA records, then one warp re-evaluates the winning super-block and
-// picks the lowest-key minimiser inside it.  Writes p.final_out.
-template <int B1, int B2, int SB, int L>
-__global__ void __launch_bounds__(1024) table_finalize_kernel(const __grid_constant__ TableParams p) {
-  constexpr int B = B1 + B2;
-  constexpr int BE = B + SB;
-  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
-  for (int i = threadIdx.x; i < p.nrec; i += 1024) {
-    const Rec r = p.cta_out[i];
-    if (rec_less(r, best)) best = r;
-  }
-  best = cta_reduce<1024>(best);
-  __shared__ Rec win;
-  if (threadIdx.x == 0) win = best;
-  __syncthreads();
-  if (threadIdx.x >= 32) return;
-  best = win;
-  const int lane = threadIdx.x;
-  if (best.val == LLONG_MAX) {
-    if (lane == 0) *p.final_out = FinalOut{LLONG_MAX, ~0ull, 0ull, 0ull, 0u, 0};
-    return;
-  }
-  const unsigned long long s = chunk_prefix(p, best.c);
-  int dir;
-  (void)chunk_key(p, s, dir);
-  const unsigned long long xo = (s << L) | ((unsigned long long)(best.j ^ (best.j >> 1)) << BE);
-  unsigned int bk = ~0u, bz = 0u;
-  const unsigned int jj = best.j;
-  const long long target = best.val;
-  for_block_states<B, SB, L>(p, xo, lane, 32, [&](unsigned int zb, long long val) {
-    if (val == target) {
-      const unsigned int kin = inner_key(p, dir, jj, zb, BE);
-      if (kin < bk) { bk = kin; bz = zb; }
-    }
-  });
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const unsigned int ok = __shfl_xor_sync(0xffffffffu, bk, off);
-    const unsigned int oz = __shfl_xor_sync(0xffffffffu, bz, off);
-    if (ok < bk) { bk = ok; bz = oz; }
-  }
-  if (lane == 0)
-    *p.final_out = FinalOut{best.val, (best.K << BE) | bk, xo | bz, best.c, best.j, bk != ~0u ? 1 : 0};
 }
 
 }  // namespace qb
