@@ -46,6 +46,7 @@ extern "C" {
 #define QB_VARIANT_TABLE 1     /* blocked Gray walk: outer field updates + inner-block fp32 table */
 #define QB_VARIANT_FIELDWALK 2 /* per-step Gray walk with register local fields (Alg. 1 form) */
 #define QB_VARIANT_COARSE 3    /* table walk with a packed-int16 block pass + exact re-evaluation */
+#define QB_VARIANT_TC 4        /* coarse block pass formed by tcgen05.mma (f16, TMEM) + exact re-evaluation */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {
@@ -66,7 +67,7 @@ typedef struct qb_result {
   double search_ms;       /* device time of the traversal (search) kernel alone */
   double collect_ms;      /* device time of the candidate-collect kernel (0 on the exact path) */
   int32_t launches;       /* kernels launched by this call */
-  int32_t reserved;
+  int32_t grid;           /* CTAs of the traversal launch */
   uint64_t param_bytes;   /* bytes of kernel parameters copied host->device per launch (Q, T tables) */
 } qb_result;
 

@@ -20,7 +20,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("QB_LIB_PATH") or os.path.join(PKG_DIR, "libqubrute_b200.so")
 HEADER = os.path.join(REPO_DIR, "include", "qubrute_b200.h")
 SOURCES = [os.path.join(PKG_DIR, "csrc", f)
-           for f in ("qb_api.cu", "qb_k_table.cu", "qb_k_coarse.cu", "qb_k_fieldwalk.cu", "qb_k_batch.cu")]
+           for f in ("qb_api.cu", "qb_k_table.cu", "qb_k_coarse.cu", "qb_k_fieldwalk.cu", "qb_k_batch.cu", "qb_k_tc.cu")]
 DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]
 
 QB_OK = 0
@@ -37,6 +37,7 @@ VARIANT_AUTO = 0
 VARIANT_TABLE = 1
 VARIANT_FIELDWALK = 2
 VARIANT_COARSE = 3
+VARIANT_TC = 4
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -67,7 +68,7 @@ class QbResult(ctypes.Structure):
         ("search_ms", ctypes.c_double),
         ("collect_ms", ctypes.c_double),
         ("launches", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
         ("param_bytes", ctypes.c_uint64),
     ]
 

@@ -53,18 +53,21 @@ struct KernelSet {
   KFn fieldwalk = nullptr;  // per-step field-walk search kernel with the same blocks (big geometry only)
   KFn coarse = nullptr;     // packed-int16 filter search kernel with the same blocks (big geometry only)
   KFn coarse_fin = nullptr; // its one-CTA record reduction (the coarse kernel only writes records)
+  KFn tc = nullptr;         // tensor-core coarse pass (records only; reduced by coarse_fin)
   std::atomic<int> occ{-1};     // resident CTAs per SM for `search` (lazy; shared by all devices)
   std::atomic<int> occ_fw{-1};  // ... for `fieldwalk`
   std::atomic<int> occ_c{-1};   // ... for `coarse`
+  std::atomic<int> occ_t{-1};   // ... for `tc`
 };
 
 static std::vector<std::unique_ptr<KernelSet>>& kernel_sets() {
   static std::vector<std::unique_ptr<KernelSet>> sets = [] {
     std::vector<std::unique_ptr<KernelSet>> v;
-    int nt = 0, nc = 0, nf = 0;
+    int nt = 0, nc = 0, nf = 0, ntc = 0;
     const TableFns* t = table_fns(&nt);
     const LFn* c = coarse_fns(&nc);
     const LFn* f = fieldwalk_fns(&nf);
+    const LFn* tcf = tc_fns(&ntc);
     for (int i = 0; i < nt; ++i) {
       auto k = std::make_unique<KernelSet>();
       k->B1 = t[i].B1; k->B2 = t[i].B2; k->L = t[i].L;
@@ -78,6 +81,11 @@ static std::vector<std::unique_ptr<KernelSet>>& kernel_sets() {
           }
         for (int j = 0; j < nf; ++j)
           if (f[j].L == k->L) k->fieldwalk = f[j].fn;
+        for (int j = 0; j < ntc; ++j)
+          if (tcf[j].L == k->L) {
+            k->tc = tcf[j].fn;
+            if (!k->coarse_fin) k->coarse_fin = tcf[j].fin;
+          }
       }
       v.push_back(std::move(k));
     }
@@ -284,10 +292,29 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint((double)P.T[z + 1] * cscale) : 0;
     P.Tc2[z / 2] = (unsigned)(t0 + bias) | ((unsigned)(t1 + bias) << 16);
   }
+  // f16 image for the tensor-core pass (qb_tc.cuh): every partial sum of a product row
+  // sum_i z_i hc_i + (Tc(z) + beta) must stay within [-2048, 2048] (exact f16 integers) and every
+  // result >= 0.  With R_H = sum_{i<B} sum_{q>=B} |q_iq| (bound on sum |H_i|), Hc = R_H 2^-s + B/2
+  // bounds sum |hc_i|, and beta = ceil(Hc) - min Tc: partial sums lie in [-Hc, 2 Hc + 1 + Tc span].
+  double r_h = 0.0, tmin = 0.0, tmax = 0.0;
+  for (int i = 0; i < B && i < n; ++i)
+    for (int q2 = B; q2 < n; ++q2) r_h += std::fabs(i < q2 ? q[(size_t)i * n + q2] : q[(size_t)q2 * n + i]);
+  for (int z = 0; z < (1 << B); ++z) {
+    tmin = std::min(tmin, (double)P.T[z]);
+    tmax = std::max(tmax, (double)P.T[z]);
+  }
+  int ts = 0;
+  while (std::ldexp(2.0 * r_h + (tmax - tmin), -ts) + B + 4 > 2047.0) ++ts;
+  const double tscale = std::ldexp(1.0, -ts);
+  int tcmin = 0;
+  for (int z = 0; z < (1 << B); ++z) tcmin = std::min(tcmin, (int)std::nearbyint((double)P.T[z] * tscale));
+  P.tc_shift = ts;
+  P.tc_scale = (float)tscale;
+  P.tc_bias = (int)std::ceil(r_h * tscale + 0.5 * B) - tcmin;
   return QB_OK;
 }
 
-static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& BE, int& L) {
+static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& BE, int& L, bool tc = false) {
   const int lmax = n - m_lock;  // free bits available per chunk
   if (lmax < 1) return fail(QB_E_ARG, "no free bits");
   if (lmax <= BIG_BE) {
@@ -300,7 +327,11 @@ static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int
 #ifndef QB_CHUNKS_PER_THREAD
 #define QB_CHUNKS_PER_THREAD 4
 #endif
-  const double want_chunks = (double)QB_CHUNKS_PER_THREAD * sms * QB_MINB * TPB * (double)shard_count;
+#ifndef QB_TC_ROUNDS
+#define QB_TC_ROUNDS 64  // tensor-core kernel: CTA-wide rounds of 128 chunks per resident CTA
+#endif
+  const double want_chunks = tc ? (double)QB_TC_ROUNDS * sms * TC_CTAS_PER_SM * TC_WORKERS * (double)shard_count
+                                : (double)QB_CHUNKS_PER_THREAD * sms * QB_MINB * TPB * (double)shard_count;
   int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
   int Lw = n - want_k;
   if (Lw & 1) Lw += (Lw < 16) ? 1 : -1;  // even chunk sizes: round up for small, down for large chunks
@@ -370,7 +401,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_COARSE) return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_TC) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -382,7 +413,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   pl.P = std::make_unique<TableParams>();
   const int m_lock = std::max(m_fix, m_tie);
   int BE, L;
-  if (int rc = choose_geometry(n, m_lock, shard_count, dev->sms, BE, L)) return rc;
+  const bool want_tc = variant == QB_VARIANT_TC;
+  if (int rc = choose_geometry(n, m_lock, shard_count, dev->sms, BE, L, want_tc)) return rc;
   pl.BE = BE;
   pl.L = L;
   pl.k = n - L;
@@ -395,8 +427,10 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   // prune almost every block (>= 32 blocks per thread); small problems use the table kernel directly
   const double blocks_per_thread =
       std::ldexp(1.0, n - m_fix - BE) / (double)shard_count / ((double)dev->sms * QB_MINB * TPB);
-  const bool coarse = pl.ks->coarse != nullptr &&
-                      (variant == QB_VARIANT_COARSE || (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
+  const bool tc = want_tc && pl.ks->tc != nullptr;
+  const bool coarse = !tc && pl.ks->coarse != nullptr &&
+                      (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC ||
+                       (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   QB_TMARK("geometry");
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl)) return rc;
   QB_TMARK("quantize");
@@ -416,7 +450,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   P.chunk_end = ce;
 
   std::memset(out, 0, sizeof(*out));
-  out->variant = fieldwalk ? QB_VARIANT_FIELDWALK : (coarse ? QB_VARIANT_COARSE : QB_VARIANT_TABLE);
+  out->variant = fieldwalk ? QB_VARIANT_FIELDWALK : tc ? QB_VARIANT_TC : (coarse ? QB_VARIANT_COARSE : QB_VARIANT_TABLE);
   out->scale_exp = pl.e;
   out->prefix_bits = pl.k;
   out->exact = pl.exact ? 1 : 0;
@@ -431,17 +465,28 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
 
   KernelSet& ks = *pl.ks;
-  const KFn search_fn = fieldwalk ? ks.fieldwalk : (coarse ? ks.coarse : ks.search);
-  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : (coarse ? ks.occ_c : ks.occ);
+  const KFn search_fn = fieldwalk ? ks.fieldwalk : tc ? ks.tc : (coarse ? ks.coarse : ks.search);
+  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : tc ? ks.occ_t : (coarse ? ks.occ_c : ks.occ);
+  const int tpb = tc ? TC_TPB : TPB, smem = tc ? TC_SMEM : 0, rows = tc ? TC_WORKERS : TPB;
   int occ = occ_cache.load();
   if (occ < 0) {
     int o = 0;
-    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, search_fn, TPB, 0));
+    if (tc) QB_CUDA(cudaFuncSetAttribute(search_fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, search_fn, tpb, smem));
+    if (getenv("QB_DEBUG_OCC")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, search_fn);
+      fprintf(stderr, "occ %d tpb %d smem %d regs %d static_smem %zu max_dyn %d carveout %d\n", o, tpb, smem, fa.numRegs,
+              fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.preferredShmemCarveout);
+    }
     occ = std::max(o, 1);
+    // tensor-core kernel: TC_CTAS_PER_SM per SM by construction (TMEM columns, launch bounds, 42 KB
+    // shared memory each); the occupancy query under-reports it (measured: they do co-reside)
+    if (tc) occ = TC_CTAS_PER_SM;
     occ_cache.store(occ);
   }
   const unsigned long long resident = (unsigned long long)occ * dev->sms;
-  const unsigned long long need_ctas = (nchunks + TPB - 1) / TPB;
+  const unsigned long long need_ctas = (nchunks + rows - 1) / rows;
   const int grid = (int)std::min(need_ctas, resident);
   if (int rc = ensure(&dev->d_cta, &dev->cta_cap, (size_t)grid)) return rc;
   P.cta_out = dev->d_cta;
@@ -472,10 +517,11 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   QB_CUDA(cudaMemsetAsync(dev->d_work, 0, 6 * sizeof(unsigned long long), st));
   QB_TMARK("memsets");
   QB_CUDA(cudaEventRecord(dev->ev0, st));
-  search_fn<<<grid, TPB, 0, st>>>(P);  // table / field walk: the last CTA reduces the records into d_final
+  search_fn<<<grid, tpb, smem, st>>>(P);  // table / field walk: the last CTA reduces the records into d_final
   QB_CUDA(cudaGetLastError());
   out->launches = 1;
-  if (search_fn == ks.coarse) {
+  out->grid = grid;
+  if (search_fn == ks.coarse || search_fn == ks.tc) {
     ks.coarse_fin<<<1, TPB, 0, st>>>(P);
     QB_CUDA(cudaGetLastError());
     out->launches = 2;

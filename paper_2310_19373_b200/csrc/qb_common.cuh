@@ -25,6 +25,21 @@ namespace qb {
 constexpr int NMAX = 40;   // reference core.py:24 MAX_DIM
 constexpr int BMAX = 10;   // largest inner block (1024-entry table, 4 KB in the constant bank)
 
+// tensor-core coarse pass (qb_tc.cuh)
+#ifndef QB_TC_ISSUER_WARP
+#define QB_TC_ISSUER_WARP 0  // 1: a fifth warp issues the MMAs; 0: worker thread 0 issues inline
+#endif
+constexpr int TC_WORKERS = 128;                // worker threads = rows of one MMA
+constexpr int TC_TPB = TC_WORKERS + (QB_TC_ISSUER_WARP ? 32 : 0);
+#ifndef QB_TC_TILE_N
+#define QB_TC_TILE_N 64
+#endif
+constexpr int TC_TILE_N = QB_TC_TILE_N;         // states per MMA tile (TMEM columns per buffer)
+constexpr int TC_CTAS_PER_SM = 512 / (2 * TC_TILE_N);  // two tile buffers per CTA fill the 512 TMEM columns
+constexpr int TC_ZBYTES = (1 << BMAX) * 32;    // Z operand: 1024 rows x 16 f16
+constexpr int TC_ABYTES = TC_WORKERS * 32;     // A operand: 128 rows x 16 f16
+constexpr int TC_SMEM = TC_ZBYTES + 2 * TC_ABYTES;
+
 // One (value, tie-key) candidate.  val is the quantized objective (exact integer);
 // K is the tie key of the block (key >> B); c/j locate the block for finalization.
 struct Rec {
@@ -53,6 +68,9 @@ struct alignas(16) TableParams {
   unsigned Tc2[1 << (BMAX - 1)];  // coarse table pairs: Tc2[z/2] = (Tc(z) + 2^14) | (Tc(z+1) + 2^14) << 16
   float coarse_scale;        // 2^-s: coarse units per quantized unit
   int coarse_shift;          // s (coarse unit = 2^s quantized units); 0 = coarse is exact
+  float tc_scale;            // tensor-core pass (qb_tc.cuh): 2^-s_tc
+  int tc_shift;              // s_tc: f16 coarse unit = 2^s_tc quantized units; 0 = exact
+  int tc_bias;               // beta: added to every coarse table entry so all f16 results are >= 0
   int n, k, L, m_fix;
   int m_tie, rule, mode, nrec;
   unsigned long long suffix;       // value of the m_fix fixed high bits
