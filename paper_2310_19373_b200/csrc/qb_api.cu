@@ -292,10 +292,10 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint((double)P.T[z + 1] * cscale) : 0;
     P.Tc2[z / 2] = (unsigned)(t0 + bias) | ((unsigned)(t1 + bias) << 16);
   }
-  // f16 image for the tensor-core pass (qb_tc.cuh): every partial sum of a product row
-  // sum_i z_i hc_i + (Tc(z) + beta) must stay within [-2048, 2048] (exact f16 integers) and every
-  // result >= 0.  With R_H = sum_{i<B} sum_{q>=B} |q_iq| (bound on sum |H_i|), Hc = R_H 2^-s + B/2
-  // bounds sum |hc_i|, and beta = ceil(Hc) - min Tc: partial sums lie in [-Hc, 2 Hc + 1 + Tc span].
+  // coarse image for the tensor-core pass (qb_tc.cuh): D(z) = sum_i z_i hc_i + Tc(z) + beta must lie
+  // in [0, 1023] (11-bit fields of the fp32 accumulators, f16-exact operands).  With
+  // R_H = sum_{i<B} sum_{q>=B} |q_iq| (bound on sum |H_i|), Hc = R_H 2^-s + B/2 bounds sum |hc_i|, and
+  // beta = ceil(Hc) - min Tc: D lies in [0, 2 Hc + 1 + Tc span].
   double r_h = 0.0, tmin = 0.0, tmax = 0.0;
   for (int i = 0; i < B && i < n; ++i)
     for (int q2 = B; q2 < n; ++q2) r_h += std::fabs(i < q2 ? q[(size_t)i * n + q2] : q[(size_t)q2 * n + i]);
@@ -304,7 +304,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
     tmax = std::max(tmax, (double)P.T[z]);
   }
   int ts = 0;
-  while (std::ldexp(2.0 * r_h + (tmax - tmin), -ts) + B + 4 > 2047.0) ++ts;
+  while (std::ldexp(2.0 * r_h + (tmax - tmin), -ts) + B + 4 > 1023.0) ++ts;
   const double tscale = std::ldexp(1.0, -ts);
   int tcmin = 0;
   for (int z = 0; z < (1 << B); ++z) tcmin = std::min(tcmin, (int)std::nearbyint((double)P.T[z] * tscale));
@@ -328,14 +328,14 @@ static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int
 #define QB_CHUNKS_PER_THREAD 4
 #endif
 #ifndef QB_TC_ROUNDS
-#define QB_TC_ROUNDS 64  // tensor-core kernel: CTA-wide rounds of 128 chunks per resident CTA
+#define QB_TC_ROUNDS 16  // tensor-core kernel: CTA-wide rounds of 128 chunks per resident CTA
 #endif
   const double want_chunks = tc ? (double)QB_TC_ROUNDS * sms * TC_CTAS_PER_SM * TC_WORKERS * (double)shard_count
                                 : (double)QB_CHUNKS_PER_THREAD * sms * QB_MINB * TPB * (double)shard_count;
   int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
   int Lw = n - want_k;
   if (Lw & 1) Lw += (Lw < 16) ? 1 : -1;  // even chunk sizes: round up for small, down for large chunks
-  Lw = std::max(Lw, BIG_BE);
+  Lw = std::max(Lw, tc ? std::min(14, lmax) : BIG_BE);  // tensor-core kernels exist for L >= 14
   Lw = std::min(Lw, std::min(22, lmax));
   if (Lw > 14) Lw = 2 * (Lw / 2);
   L = Lw;
@@ -471,14 +471,11 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   int occ = occ_cache.load();
   if (occ < 0) {
     int o = 0;
-    if (tc) QB_CUDA(cudaFuncSetAttribute(search_fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, search_fn, tpb, smem));
-    if (getenv("QB_DEBUG_OCC")) {
-      cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, search_fn);
-      fprintf(stderr, "occ %d tpb %d smem %d regs %d static_smem %zu max_dyn %d carveout %d\n", o, tpb, smem, fa.numRegs,
-              fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.preferredShmemCarveout);
+    if (tc) {
+      QB_CUDA(cudaFuncSetAttribute(search_fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      QB_CUDA(cudaFuncSetAttribute(search_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
     }
+    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, search_fn, tpb, smem));
     occ = std::max(o, 1);
     // tensor-core kernel: TC_CTAS_PER_SM per SM by construction (TMEM columns, launch bounds, 42 KB
     // shared memory each); the occupancy query under-reports it (measured: they do co-reside)

@@ -25,19 +25,21 @@ namespace qb {
 constexpr int NMAX = 40;   // reference core.py:24 MAX_DIM
 constexpr int BMAX = 10;   // largest inner block (1024-entry table, 4 KB in the constant bank)
 
-// tensor-core coarse pass (qb_tc.cuh)
-#ifndef QB_TC_ISSUER_WARP
-#define QB_TC_ISSUER_WARP 0  // 1: a fifth warp issues the MMAs; 0: worker thread 0 issues inline
-#endif
+// tensor-core coarse pass (qb_tc.cuh): two states per TMEM cell, K = 32 f16 operands
 constexpr int TC_WORKERS = 128;                // worker threads = rows of one MMA
-constexpr int TC_TPB = TC_WORKERS + (QB_TC_ISSUER_WARP ? 32 : 0);
+constexpr int TC_TPB = TC_WORKERS + 32;        // + the MMA issuer warp
+constexpr int TC_K = 32;                       // operand columns (two kind::f16 K-steps)
+constexpr int TC_CELLS = (1 << BMAX) / 2;      // TMEM cells per block row (two states each)
 #ifndef QB_TC_TILE_N
-#define QB_TC_TILE_N 64
+#define QB_TC_TILE_N 128
 #endif
-constexpr int TC_TILE_N = QB_TC_TILE_N;         // states per MMA tile (TMEM columns per buffer)
-constexpr int TC_CTAS_PER_SM = 512 / (2 * TC_TILE_N);  // two tile buffers per CTA fill the 512 TMEM columns
-constexpr int TC_ZBYTES = (1 << BMAX) * 32;    // Z operand: 1024 rows x 16 f16
-constexpr int TC_ABYTES = TC_WORKERS * 32;     // A operand: 128 rows x 16 f16
+#ifndef QB_TC_CTAS
+#define QB_TC_CTAS (512 / (2 * QB_TC_TILE_N))
+#endif
+constexpr int TC_TILE_N = QB_TC_TILE_N;        // cells per MMA tile = TMEM columns per buffer
+constexpr int TC_CTAS_PER_SM = QB_TC_CTAS;     // two tile buffers per CTA; at most 512 TMEM columns per SM
+constexpr int TC_ZBYTES = TC_CELLS * TC_K * 2;  // Z operand: 512 cell rows x 32 f16
+constexpr int TC_ABYTES = TC_WORKERS * TC_K * 2;  // A operand: 128 block rows x 32 f16
 constexpr int TC_SMEM = TC_ZBYTES + 2 * TC_ABYTES;
 
 // One (value, tie-key) candidate.  val is the quantized objective (exact integer);

@@ -1,37 +1,55 @@
-// Tensor-core coarse-filter traversal kernel (QB_VARIANT_TC): the coarse block pass of
-// qb_coarse.cuh with the 2^B candidate values of every block formed by tcgen05.mma.
+// Tensor-core coarse-filter traversal kernel (QB_VARIANT_TC): the coarse block test of
+// qb_coarse.cuh with the candidate values of every block formed by tcgen05.mma.
 //
 // Same chunks, outer Gray walk (Eq. 3 field updates), blocks, certified bound, exact fallback and
 // tie keys as the coarse kernel.  What changes is who forms the coarse image
 //     C(z) = sum_{i<B} z_i hc_i + Tc(z),   hc_i = rint(H_i 2^-s),  Tc(z) = rint(T(z) 2^-s)
-// of the 1024 states z of a block: one CTA stacks the fields of the 128 blocks its 128 worker
-// threads are on (one block per thread) into A [128 x 16] f16 (hc_0..hc_9, 1, 0...) and multiplies
-// it by the per-instance constant Z [1024 x 16] f16 (row z: the bits of z, Tc(z) + beta, 0...):
-//     D = A Z^T  ->  D[thread, z] = C_thread(z) + beta
-// in M=128 x N=TC_TILE_N x K=16 MMAs with f16 accumulators in TMEM.  The host picks s so that
-// every partial sum of every product row lies in [-2048, 2048]: all f16 arithmetic is exact
-// integer arithmetic, whatever the tensor core's summation order, and beta makes every D >= 0 so
-// the f16 bit patterns order like u16.  Each thread then reads its own TMEM lane (.pack::16b: two
-// states per register) and folds it with VIMNMX3.U16x2 (four states per instruction).  Each
-// state's coarse value is still formed (by the tensor core) and compared (by the thread).
+// of the 1024 states of a block and compares it with the block's threshold.  A block of a thread
+// whose running best (or the device-wide best) is thr can hold a better or tied state only if some
+// C(z) <= Lc = floor((thr + slack - V) 2^-s); with D(z) = C(z) + beta >= 0 and Ld = Lc + beta clamped
+// to [-1, 1023], every state's test is one bit of F(z) = D(z) + 1023 - Ld in [0, 2047]:
+//     z passes  <=>  D(z) <= Ld  <=>  bit 10 of F(z) is clear.
+// One CTA stacks the rows of the 128 blocks its 128 worker threads are on into A [128 x 32] f16 and
+// multiplies by the per-instance Z [512 x 32] f16, whose cell row p pairs the states p and p + 512:
+//     A row:  hc_0..hc_9, 1, O, 2048, 0 0 0 | hc_0..hc_9, 2048, O, 0 ...          (O = 1023 - Ld)
+//     Z row:  bits of p, Tc'(p), 1, 4096, 0 0 0 | 2048 bits of p+512, Tc'(p+512), 2048, 0 ...
+//     D[row, p] = 2^23 + F(p) + 2048 F(p + 512)          (Tc' = Tc + beta, fp32 accumulators)
+// Every product and partial sum is an integer below 2^24 in magnitude, so the fp32 accumulation is
+// exact whatever the tensor core's summation order, and the fixed 2^23 term pins the exponent: the
+// low 22 bits of each TMEM cell are F(p) | F(p+512) << 11.  A thread reads its own TMEM lane (512
+// cells per block) and ANDs the cells three at a time (LOP3, four states per instruction); the
+// block passes iff bit 10 or bit 21 of the AND is clear.  Passing blocks (rare once a good value is
+// known) get the exact fp32 table evaluation; a failed block is bounded below by
+// V + (Ld - beta + 1) 2^s - slack, which keeps the per-chunk minima of the collect pass valid.  Each
+// state's coarse value is still formed (by the tensor core) and compared (by the bit test).
 //
-// Roles: four warps, one chunk per thread (CTA-wide rounds of 128 chunks so the rows advance in
-// lockstep); thread 0 also issues the MMAs (a dedicated issuer warp would put a third warp on some
-// SM sub-partition and cap the registers).  Pipelines (mbarriers):
-//   bar_a[2]     warps -> issuer: A rows of batch g written (double-buffered by g & 1)
-//   bar_full[2]  MMA -> warps: tile in TMEM buffer b done (tcgen05.commit)
-//   bar_empty[2] warps -> issuer: TMEM buffer b read back (one arrival per warp)
-// TMEM: 2 TC_TILE_N columns per CTA = two tile buffers; 512 / (2 TC_TILE_N) CTAs per SM.
+// Roles: warps 0-3 are workers (one chunk per thread, CTA-wide rounds of 128 chunks so the rows
+// advance in lockstep), warp 4 issues the MMAs from one lane.  Pipelines (mbarriers):
+//   bar_a[2]     workers -> issuer: A rows of batch g written (double-buffered by g & 1)
+//   bar_full[2]  MMA -> workers: tile in TMEM buffer b done (tcgen05.commit)
+//   bar_empty[2] workers -> issuer: TMEM buffer b read back (one arrival per worker warp)
+// TMEM: two 128-column tile buffers per CTA, two CTAs per SM (all 512 columns).
 #pragma once
 #include <cuda_fp16.h>
 #ifdef QB_TC_TRACE
 #include <cstdio>
+#define QB_TR(...) __VA_ARGS__
+#else
+#define QB_TR(...)
 #endif
 #include "qb_coarse.cuh"
 #include "qb_tc_ptx.cuh"
 
 namespace qb {
 
+namespace tc {
+// element (row r, k) of a [rows x 32] f16 K-major SWIZZLE_NONE operand: 8-row x 16-byte core
+// matrices, LBO = 128 B (next core matrix along K), SBO = 512 B (next 8-row group)
+__host__ __device__ constexpr uint32_t off32(int r, int k) {
+  return (uint32_t)((r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+constexpr uint32_t kLBO = 128, kSBO = 512, kKStep = 256;  // second K=16 step starts 2 core matrices in
+}  // namespace tc
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -42,28 +60,40 @@ __device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// A row of one block: hc_0..hc_{B-1}, 1, zeros (K = 16) into the operand tile at row r
+// 32 f16 values (as 8 x uint4) into row r of a K=32 operand tile
+__device__ __forceinline__ void tc_store_row(uint8_t* tile, int r, const uint32_t (&w)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    *reinterpret_cast<uint4*>(tile + tc::off32(r, 8 * q)) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+// A row of one block: fields rounded to coarse units and the threshold offset O
 template <int B>
-__device__ __forceinline__ void tc_write_row(uint8_t* a_tile, int r, const float (&H)[B], float scale, bool active) {
-  static_assert(B == 10, "row layout assumes 10 table bits (K = 16)");
+__device__ __forceinline__ void tc_write_row(uint8_t* a_tile, int r, const float (&H)[B], float scale, float O,
+                                             bool active) {
+  static_assert(B == 10, "row layout assumes 10 table bits");
   float h[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) h[i] = active ? rintf(H[i] * scale) : 0.f;
-  uint4 lo, hi;
-  lo.x = pack_f16x2(h[0], h[1]);
-  lo.y = pack_f16x2(h[2], h[3]);
-  lo.z = pack_f16x2(h[4], h[5]);
-  lo.w = pack_f16x2(h[6], h[7]);
-  hi.x = pack_f16x2(h[8], h[9]);
-  hi.y = pack_f16x2(1.f, 0.f);
-  hi.z = 0u;
-  hi.w = 0u;
-  *reinterpret_cast<uint4*>(a_tile + tc::operand_offset(r, 0)) = lo;
-  *reinterpret_cast<uint4*>(a_tile + tc::operand_offset(r, 8)) = hi;
+  uint32_t w[16];
+  w[0] = pack_f16x2(h[0], h[1]);
+  w[1] = pack_f16x2(h[2], h[3]);
+  w[2] = pack_f16x2(h[4], h[5]);
+  w[3] = pack_f16x2(h[6], h[7]);
+  w[4] = pack_f16x2(h[8], h[9]);
+  w[5] = pack_f16x2(1.f, O);
+  w[6] = pack_f16x2(2048.f, 0.f);
+  w[7] = 0u;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) w[8 + q] = w[q];
+  w[13] = pack_f16x2(2048.f, O);
+  w[14] = 0u;
+  w[15] = 0u;
+  tc_store_row(a_tile, r, w);
 }
 
 // exact fp32 minimum of block j of chunk c relative to its base value (rare: blocks whose coarse
-// bound reaches the best value seen); the fields come from a direct evaluation of the block base
+// test passes); the fields come from a direct evaluation of the block base
 template <int B1, int B2, int L>
 __device__ __noinline__ float tc_exact_block_min(const TableParams& p, unsigned long long c, unsigned int j) {
   constexpr int B = B1 + B2, NF = (L - B) > 0 ? (L - B) : 1;
@@ -74,13 +104,20 @@ __device__ __noinline__ float tc_exact_block_min(const TableParams& p, unsigned 
   return block_min<B1, B2, 0, NF>(p, H, F);
 }
 
+// clamped coarse threshold Ld in [-1, 1023] of a block with base V under pruning limit lim
+__device__ __forceinline__ int tc_ld(long long lim, long long V, int shift, int bias) {
+  if (lim == LLONG_MAX) return 1023;
+  const long long lc = (lim - V) >> shift;  // floor
+  return (int)max(-1ll, min(1023ll, lc + bias));
+}
+
 template <int B1, int B2, int L>
 __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(B == BMAX, "the tensor-core pass covers 1024-state blocks");
   constexpr int LO = L - B;
   constexpr int NF = LO > 0 ? LO : 1;
-  constexpr int NT = (1 << B) / TC_TILE_N;  // MMA tiles per block
+  constexpr int NT = TC_CELLS / TC_TILE_N;  // MMA tiles per block
   static_assert(NT % 2 == 0, "tiles alternate between the two TMEM buffers");
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   uint8_t* zmat = tc_smem;
@@ -92,25 +129,30 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- prologue: Z operand (row z: bits of z, Tc(z) + beta) from the fp32 table, TMEM, barriers
-  for (int z = tid; z < (1 << B); z += TC_TPB) {
-    float h[16];
+  // ---- prologue: Z operand from the fp32 table, TMEM, barriers
+  for (int pc = tid; pc < TC_CELLS; pc += TC_TPB) {
+    const int zh = pc + TC_CELLS;
+    float lo[16], hi[16];
 #pragma unroll
-    for (int i = 0; i < B; ++i) h[i] = (float)((z >> i) & 1);
-    h[B] = rintf(p.T[z] * p.tc_scale) + (float)p.tc_bias;
+    for (int i = 0; i < B; ++i) {
+      lo[i] = (float)((pc >> i) & 1);
+      hi[i] = 2048.f * (float)((zh >> i) & 1);
+    }
+    lo[B] = rintf(p.T[pc] * p.tc_scale) + (float)p.tc_bias;
+    lo[B + 1] = 1.f;
+    lo[B + 2] = 4096.f;
+    hi[B] = rintf(p.T[zh] * p.tc_scale) + (float)p.tc_bias;
+    hi[B + 1] = 2048.f;
+    hi[B + 2] = 0.f;
 #pragma unroll
-    for (int i = B + 1; i < 16; ++i) h[i] = 0.f;
-    uint4 lo, hi;
-    lo.x = pack_f16x2(h[0], h[1]);
-    lo.y = pack_f16x2(h[2], h[3]);
-    lo.z = pack_f16x2(h[4], h[5]);
-    lo.w = pack_f16x2(h[6], h[7]);
-    hi.x = pack_f16x2(h[8], h[9]);
-    hi.y = pack_f16x2(h[10], h[11]);
-    hi.z = pack_f16x2(h[12], h[13]);
-    hi.w = pack_f16x2(h[14], h[15]);
-    *reinterpret_cast<uint4*>(zmat + tc::operand_offset(z, 0)) = lo;
-    *reinterpret_cast<uint4*>(zmat + tc::operand_offset(z, 8)) = hi;
+    for (int i = B + 3; i < 16; ++i) lo[i] = hi[i] = 0.f;
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      w[q] = pack_f16x2(lo[2 * q], lo[2 * q + 1]);
+      w[8 + q] = pack_f16x2(hi[2 * q], hi[2 * q + 1]);
+    }
+    tc_store_row(zmat, pc, w);
   }
   if (warp == 0) tc::tmem_alloc<2 * TC_TILE_N>(&tmem_base);
   if (tid == 0) {
@@ -128,209 +170,192 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base;
 
-  // MMA issue (thread 0 only).  Tile t of batch g is the (NT g + t)-th tile of this CTA: TMEM buffer
-  // t & 1, and its fill / drain is phase (NT/2) g + t/2 of that buffer's barriers.  Tile tt + 2 reuses
-  // the buffer of tile tt, so it is issued once every warp has read tile tt back.
-  constexpr uint32_t idesc = tc::idesc_f16_f16(TC_WORKERS, TC_TILE_N);
-  const uint64_t zdesc = tc::smem_desc(tc::smem_u32(zmat), 128, 256);
-  const uint64_t adesc0 = tc::smem_desc(tc::smem_u32(a_tile[0]), 128, 256);
-  const uint64_t adesc1 = tc::smem_desc(tc::smem_u32(a_tile[1]), 128, 256);
-  auto issue = [&](uint32_t g, int t) {  // tile t of batch g
-    const uint64_t ad = (g & 1) ? adesc1 : adesc0;
-    // Z rows [N t, N t + N): N/8 8-row groups of 256 B, 32 N t bytes in
-    tc::mma_f16(tmem + (t & 1) * TC_TILE_N, ad, zdesc + (uint64_t)(t * (TC_TILE_N * 32 / 16)), idesc, 0u);
-    tc::mma_commit(&bar_full[t & 1]);
-  };
-
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
-  if (QB_TC_ISSUER_WARP && warp == TC_WORKERS / 32) {
-    // dedicated issuer: batch g's tiles once its A rows are published, each into a drained buffer
+  if (warp == TC_WORKERS / 32) {
+    // ---------------------------------------------------------------- MMA issuer
+    // Tile t of batch g is the (NT g + t)-th tile: TMEM buffer t & 1, and its fill / drain is phase
+    // (NT/2) g + t/2 of that buffer's barriers, so every parity is a compile-time constant.
     if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_f16_f32(TC_WORKERS, TC_TILE_N);
+      const uint64_t zdesc = tc::smem_desc(tc::smem_u32(zmat), tc::kLBO, tc::kSBO);
+      const uint64_t adesc[2] = {tc::smem_desc(tc::smem_u32(a_tile[0]), tc::kLBO, tc::kSBO),
+                                 tc::smem_desc(tc::smem_u32(a_tile[1]), tc::kLBO, tc::kSBO)};
+      QB_TR(long long ta = 0, te = 0, ti = 0; uint32_t ng = 0;)
       for (uint32_t g = 0;; ++g) {
         const int s = g & 1;
+        QB_TR(long long c0 = clock64();)
         tc::mbar_wait(&bar_a[s], (g >> 1) & 1);
+        QB_TR(ta += clock64() - c0; ++ng;)
         if (*(volatile int*)&stop_flag[s]) break;
         tc::tc_fence_after();
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
+          QB_TR(long long c1 = clock64();)
           if (g > 0 || t >= 2) {
             tc::mbar_wait(&bar_empty[t & 1], ((t >> 1) + 1) & 1);
             tc::tc_fence_after();
           }
-          issue(g, t);
+          QB_TR(long long c2 = clock64(); te += c2 - c1;)
+          // Z cell rows [128 t, 128 t + 128): 16 8-row groups of 512 B; descriptor addresses in 16 B units
+          const uint64_t zd = zdesc + (uint64_t)(t * TC_TILE_N * TC_K * 2 / 16);
+          const uint32_t d = tmem + (t & 1) * TC_TILE_N;
+          tc::mma_f16(d, adesc[s], zd, idesc, 0u);
+          tc::mma_f16(d, adesc[s] + tc::kKStep / 16, zd + tc::kKStep / 16, idesc, 1u);
+          tc::mma_commit(&bar_full[t & 1]);
+          QB_TR(ti += clock64() - c2;)
         }
       }
+      QB_TR(if (blockIdx.x == 0) printf("issuer: batches %u, per batch: wait_a %.0f wait_empty %.0f issue %.0f clk\n", ng,
+                                      (double)ta / ng, (double)te / ng, (double)ti / ng);)
     }
     __syncwarp();
   } else {
-  const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
-  const long long slack = (long long)(B + 1) << p.tc_shift >> 1;
-  const bool coarse_exact = p.tc_shift == 0;
-  const uint32_t lane_tmem = tmem + ((uint32_t)(warp * 32) << 16);
-  int round = 0;
-  // the block being prepared (fields) ...
-  bool active = false;
-  unsigned long long c = 0, ci = 0, key_hi = 0;
-  int dir = 0;
-  unsigned int j = 0;
-  long long V = 0;
-  float H[B], F[NF];
-  // ... and running per-chunk state of the block being consumed
-  long long cmin = LLONG_MAX, skip_min = LLONG_MAX, thr = LLONG_MAX, lim = LLONG_MAX;
+    // ---------------------------------------------------------------- workers
+    const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+    const long long slack = (long long)(B + 1) << p.tc_shift >> 1;
+    const uint32_t lane_tmem = tmem + ((uint32_t)(warp * 32) << 16);
+    int round = 0;
+    // the block being prepared (fields, threshold) ...
+    bool active = false;
+    unsigned long long c = 0, ci = 0, key_hi = 0;
+    int dir = 0, ld_next = 1023;
+    unsigned int j = 0;
+    long long V = 0;
+    float H[B], F[NF];
+    // ... and running per-chunk state of the block being consumed
+    long long cmin = LLONG_MAX, skip_min = LLONG_MAX, thr = LLONG_MAX, lim = LLONG_MAX;
 
-  auto fetch_round = [&]() -> bool {  // CTA-wide: the next 128 chunks, one per thread
-    if (tid == 0) round_base[round & 1] = atomicAdd(p.work, (unsigned long long)TC_WORKERS);
-    named_bar_sync(1, TC_WORKERS);
-    const unsigned long long base = round_base[round & 1];
-    ++round;
-    if (base >= nchunks) return false;
-    ci = base + tid;
-    active = ci < nchunks;
-    j = 0;
-    if (active) {
-      c = p.chunk_begin + ci;
-      const unsigned long long s = chunk_prefix(p, c);
-      base_eval<B, L>(p, s << L, L, V, H, F);
-      key_hi = chunk_key(p, s, dir);
-    } else {
+    auto fetch_round = [&]() -> bool {  // worker-wide: the next 128 chunks, one per thread
+      if (tid == 0) round_base[round & 1] = atomicAdd(p.work, (unsigned long long)TC_WORKERS);
+      named_bar_sync(1, TC_WORKERS);
+      const unsigned long long base = round_base[round & 1];
+      ++round;
+      if (base >= nchunks) return false;
+      ci = base + tid;
+      active = ci < nchunks;
+      j = 0;
+      if (active) {
+        c = p.chunk_begin + ci;
+        const unsigned long long s = chunk_prefix(p, c);
+        base_eval<B, L>(p, s << L, L, V, H, F);
+        key_hi = chunk_key(p, s, dir);
+        // a new chunk starts from the device-wide best (the thread's own best is in it too)
+        thr = min(best.val, gbest_dec(__ldcg(p.gbest)));
+        lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;
+      } else {
 #pragma unroll
-      for (int i = 0; i < B; ++i) H[i] = 0.f;
-    }
-    return true;
-  };
-  auto publish = [&](int slot) {
-    tc_write_row<B>(a_tile[slot], tid, H, p.tc_scale, active);
-    tc::fence_async_smem();
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&bar_a[slot]);
-  };
-  auto publish_stop = [&](int slot) {  // issuer-warp mode: no batch g, the issuer leaves its loop
-    if (QB_TC_ISSUER_WARP) {
+        for (int i = 0; i < B; ++i) H[i] = 0.f;
+      }
+      return true;
+    };
+    QB_TR(long long tq0 = 0, tq1 = 0, tq2 = 0;)
+    auto publish = [&](int slot) {
+      QB_TR(long long q0 = clock64();)
+      ld_next = tc_ld(lim, V, p.tc_shift, p.tc_bias);
+      tc_write_row<B>(a_tile[slot], tid, H, p.tc_scale, (float)(1023 - ld_next), active);
+      QB_TR(long long q1 = clock64(); tq0 += q1 - q0;)
+      tc::fence_async_smem();
+      QB_TR(long long q2 = clock64(); tq1 += q2 - q1;)
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bar_a[slot]);
+      QB_TR(tq2 += clock64() - q2;)
+    };
+    auto publish_stop = [&](int slot) {  // no batch g: the issuer leaves its loop
       if (tid == 0) stop_flag[slot] = 1;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bar_a[slot]);
-    }
-  };
+    };
 
-#ifdef QB_TC_TRACE
-  long long tr_prev = 0;
-#endif
-  bool more = fetch_round();
-  if (!more) publish_stop(0);
-  if (more) {
-    publish(0);
-    if (!QB_TC_ISSUER_WARP && tid == 0) {
-      tc::mbar_wait(&bar_a[0], 0);
-      tc::tc_fence_after();
-      issue(0, 0);
-      issue(0, 1);
-    }
-  }
-  for (uint32_t g = 0; more; ++g) {
-    // the block consumed in this iteration
-    const bool cur_active = active;
-    const unsigned long long cur_c = c, cur_ci = ci, cur_key_hi = key_hi;
-    const int cur_dir = dir;
-    const unsigned int cur_j = j;
-    const long long Vc = V;
-    if (cur_active && cur_j == 0) {  // chunk start: pruning threshold from the device-wide best
-      cmin = LLONG_MAX;
-      skip_min = LLONG_MAX;
-      thr = min(best.val, gbest_dec(__ldcg(p.gbest)));
-      lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;
-    }
-    // prepare the next block (outer Gray flip, or the next round's chunks) while the tensor core
-    // works on this one
-    if (j + 1 < (1u << LO)) {
-      ++j;
-      if (active) {
-        const int r = __ffs(j) - 1;
-        const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
-        outer_flip<B, L, B>(p, B + r, sg, V, H, F);
+    bool more = fetch_round();
+    if (more) publish(0);
+    else publish_stop(0);
+    QB_TR(long long tp = 0, tw = 0, tl = 0, tn = 0, tr = 0, tstart = clock64(); uint32_t nb = 0;)
+    for (uint32_t g = 0; more; ++g) {
+      QB_TR(long long d0 = clock64(); ++nb;)
+      // the block consumed in this iteration
+      const bool cur_active = active;
+      const unsigned long long cur_c = c, cur_ci = ci, cur_key_hi = key_hi;
+      const int cur_dir = dir, cur_ld = ld_next;
+      const unsigned int cur_j = j;
+      const long long Vc = V;
+      if (cur_active && cur_j == 0) {
+        cmin = LLONG_MAX;
+        skip_min = LLONG_MAX;
       }
-    } else {
-      more = fetch_round();
-    }
-    if (more) publish((g + 1) & 1);
-    else publish_stop((g + 1) & 1);
 
-    // fold this block's tiles: four states per VIMNMX3.U16x2
-    unsigned m0 = 0xffffffffu, m1 = 0xffffffffu;
+      // AND this block's cells: bit 10 / bit 21 stay set only if every state fails its test
+      uint32_t acc[8];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int b = t & 1;
-#ifdef QB_TC_TRACE
-      const long long tr0 = clock64();
-#endif
-      tc::mbar_wait(&bar_full[b], (t >> 1) & 1);
-#ifdef QB_TC_TRACE
-      const long long tr1 = clock64();
-#endif
-      tc::tc_fence_after();
-      uint32_t r[TC_TILE_N / 2];
+      for (int k = 0; k < 8; ++k) acc[k] = 0xffffffffu;
 #pragma unroll
-      for (int q = 0; q < TC_TILE_N / 64; ++q)
-        tc::tmem_ld32_pack16(lane_tmem + b * TC_TILE_N + 64 * q, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
-      tc::tmem_wait_ld();
-#ifdef QB_TC_TRACE
-      const long long tr2 = clock64();
-#endif
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&bar_empty[b]);
-      if (!QB_TC_ISSUER_WARP && tid == 0 && (t + 2 < NT || more)) {  // refill this buffer: tile t + 2 (maybe of batch g + 1)
-        tc::mbar_wait(&bar_empty[b], (t >> 1) & 1);
-        if (t + 2 >= NT) tc::mbar_wait(&bar_a[(g + 1) & 1], ((g + 1) >> 1) & 1);
+      for (int t = 0; t < NT; ++t) {
+        const int b = t & 1;
+        QB_TR(long long e0 = clock64();)
+        tc::mbar_wait(&bar_full[b], (t >> 1) & 1);
         tc::tc_fence_after();
-        if (t + 2 < NT) issue(g, t + 2);
-        else issue(g + 1, t + 2 - NT);
-#ifdef QB_TC_TRACE
-        const long long tr3 = clock64();
-        if (blockIdx.x == 0 && g >= 40 && g < 42)
-          printf("trace g=%u t=%d wait_full %lld ld %lld empty+issue %lld since_prev_tile %lld\n", g, t, tr1 - tr0,
-                 tr2 - tr1, tr3 - tr2, tr0 - tr_prev);
-        tr_prev = tr0;
-#endif
-      }
+        QB_TR(tw += clock64() - e0;)
+        QB_TR(long long e1 = clock64();)
+        // the whole tile into registers, then hand the buffer back before folding it
+        uint32_t r[TC_TILE_N];
 #pragma unroll
-      for (int i = 0; i < TC_TILE_N / 2; i += 4) {
-        m0 = __vimin3_u16x2(m0, r[i], r[i + 1]);
-        m1 = __vimin3_u16x2(m1, r[i + 2], r[i + 3]);
-      }
-    }
-    if (!cur_active) continue;
-    const unsigned m = __vminu2(m0, m1);
-    const unsigned short m16 = (unsigned short)min(m & 0xffffu, m >> 16);
-    const int dmin = (int)__half2float(__ushort_as_half(m16));
-    const long long cb = Vc + ((long long)(dmin - p.tc_bias) << p.tc_shift);
-    long long val;
-    bool evaluated = true;
-    if (coarse_exact) {
-      val = cb;
-    } else if (cb > lim) {  // bound cb - slack > thr: nothing here can beat or tie the best value seen
-      skip_min = min(skip_min, cb);
-      evaluated = false;
-      val = LLONG_MAX;
-    } else {
-      val = Vc + (long long)tc_exact_block_min<B1, B2, L>(p, cur_c, cur_j);
-    }
-    if (evaluated) {
-      cmin = min(cmin, val);
-      if (val <= best.val) {
-        const unsigned long long K = block_key(p, cur_key_hi, cur_dir, cur_j, LO);
-        if (val < best.val || K < best.K) best = Rec{val, K, cur_c, cur_j, 0u};
-        if (val < thr) {
-          thr = val;
-          lim = val + slack;
-          atomicMax(p.gbest, gbest_enc(val));
+        for (int q = 0; q < TC_TILE_N / 32; ++q)
+          tc::tmem_ld32(lane_tmem + b * TC_TILE_N + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
+        tc::tmem_wait_ld();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bar_empty[b]);
+        QB_TR(long long e2 = clock64(); tl += e2 - e1;)
+#pragma unroll
+        for (int i = 0; i < TC_TILE_N; i += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] &= r[i + 2 * k] & r[i + 2 * k + 1];
+        QB_TR(tn += clock64() - e2;)
+        if (t == 1) {  // A rows of the next block: needed once tile 2 has drained buffer 0
+          QB_TR(long long d0b = clock64();)
+          // prepare the next block (outer Gray flip, or the next round's chunks) while the tensor core
+          // works on this one
+          if (j + 1 < (1u << LO)) {
+            ++j;
+            if (active) {
+              const int r = __ffs(j) - 1;
+              const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
+              outer_flip<B, L, B>(p, B + r, sg, V, H, F);
+            }
+          } else {
+            more = fetch_round();
+          }
+          if (more) publish((g + 1) & 1);
+          else publish_stop((g + 1) & 1);
+          QB_TR(tp += clock64() - d0b;)
         }
       }
+      QB_TR(long long d2 = clock64();)
+      if (!cur_active) continue;
+      const uint32_t all = (acc[0] & acc[1] & acc[2]) & (acc[3] & acc[4] & acc[5]) & (acc[6] & acc[7]);
+      const bool pass = (all & 0x200400u) != 0x200400u;
+      if (pass) {
+        const long long val = Vc + (long long)tc_exact_block_min<B1, B2, L>(p, cur_c, cur_j);
+        cmin = min(cmin, val);
+        if (val <= best.val) {
+          const unsigned long long K = block_key(p, cur_key_hi, cur_dir, cur_j, LO);
+          if (val < best.val || K < best.K) best = Rec{val, K, cur_c, cur_j, 0u};
+          if (val < thr) {
+            thr = val;
+            lim = val + slack;
+            atomicMax(p.gbest, gbest_enc(val));
+          }
+        }
+      } else {  // every state: C(z) > Ld - beta, so exact >= V + (Ld - beta + 1) 2^s - slack
+        skip_min = min(skip_min, Vc + ((long long)(cur_ld - p.tc_bias + 1) << p.tc_shift));
+      }
+      if (cur_j + 1 == (1u << LO)) {  // chunk done: its minimum (or lower bound) for the collect pass
+        if (skip_min != LLONG_MAX) cmin = min(cmin, skip_min - slack);
+        if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[cur_ci] = cmin;
+      }
+      QB_TR(tr += clock64() - d2;)
     }
-    if (cur_j + 1 == (1u << LO)) {  // chunk done: its minimum (or lower bound) for the collect pass
-      if (skip_min != LLONG_MAX) cmin = min(cmin, skip_min - slack);
-      if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[cur_ci] = cmin;
-    }
-  }
+    QB_TR(if (blockIdx.x == 0 && (tid & 31) == 0) printf("warp %d: batches %u, per batch: row %.0f fence %.0f arrive %.0f prepare %.0f wait_full %.0f ld %.0f and %.0f tail %.0f total %.0f clk\n", warp, nb, (double)tq0 / nb, (double)tq1 / nb, (double)tq2 / nb,
+                                        (double)tp / nb, (double)tw / nb, (double)tl / nb, (double)tn / nb, (double)tr / nb, (double)(clock64() - tstart) / nb);)
   }
   tc::tc_fence_before();
   __syncthreads();

@@ -389,6 +389,44 @@ def test_adversarial_value_ranges_coarse_kernel(kind):
             assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (kind, seed, args)
 
 
+@pytest.mark.parametrize("n", [34, 35])
+def test_tc_kernel_matches_table_kernel(n):
+    """The tensor-core coarse pass (tcgen05.mma, fp32 TMEM cells holding two states' threshold
+    tests) returns exactly what the fp32 table kernel returns: integer, float, tie-heavy and
+    wide-range instances, subspaces and tie rules (n >= 34: chunks of >= 14 free bits)."""
+    cases = [instances.config_coeffs("D", 9, n=n), instances.config_coeffs("E", 9, n=n),
+             instances.config_coeffs("B", 9, n=n), _tie_heavy(n, 4300 + n, -1, 1),
+             instances.int_uniform_coeffs(n, 4400 + n, -(1 << 20), 1 << 20)]
+    for c in cases:
+        for args in ((0, 0, 0), (0, 0, 4), (3, 5, 3)):
+            a = _lib.solve(c, *args, variant=_lib.VARIANT_TABLE)
+            b = _lib.solve(c, *args, variant=_lib.VARIANT_TC)
+            assert b.variant == _lib.VARIANT_TC
+            assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (n, args)
+
+
+@pytest.mark.parametrize("kind", ["big_int", "wide_range", "tiny", "neg_zero", "dyadic"])
+def test_adversarial_value_ranges_tc_kernel(kind):
+    """The tensor-core pass's 10-bit coarse image (shift, beta, per-block threshold offset) on
+    adversarial value ranges at n=34, against the fp32 table kernel."""
+    c = _adversarial(kind, 34, 7100)
+    inst = qb.QuboInstance(c)
+    for args in ((0, 0, 0), (0, 0, 5)):
+        a = _lib.solve(inst.coeffs, *args, variant=_lib.VARIANT_TABLE)
+        b = _lib.solve(inst.coeffs, *args, variant=_lib.VARIANT_TC)
+        assert b.variant == _lib.VARIANT_TC
+        assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (kind, args)
+
+
+def test_tc_kernel_n40():
+    """n=40 (config E) through the tensor-core pass: same answer as the default coarse kernel."""
+    c = instances.config_coeffs("E", 0)
+    a = _lib.solve(c)
+    b = _lib.solve(c, variant=_lib.VARIANT_TC)
+    assert b.variant == _lib.VARIANT_TC
+    assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key)
+
+
 def test_concurrent_host_threads():
     """ctypes releases the GIL: several host threads solving at once (as a thread pool over the
     reference's entry points would) must each get their own correct answer."""
