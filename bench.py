@@ -385,16 +385,16 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_extra:
         line["configs"] = extra_configs(qb, _lib, instances)
-        # the other traversal kernels on the same workload: the fp32 table kernel and the literal
-        # per-step field walk (QB_VARIANT_TABLE / QB_VARIANT_FIELDWALK)
-        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse"}
+        # the other traversal kernels on the same workload: the fp32 table kernel, the literal
+        # per-step field walk and the tensor-core coarse pass (QB_VARIANT_TABLE / _FIELDWALK / _TC)
+        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse", 4: "tc"}
         line["variants"] = {f"{names[int(r.variant)]} (default)": {
             "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
-        for var in (_lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK):
+        for var in (_lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK, _lib.VARIANT_TC):
             _lib.solve(inst.coeffs, variant=var)
             vr = _lib.solve(inst.coeffs, variant=var)
             vs = states / (vr.search_ms * 1e-3)
-            line["variants"][names[var]] = {"search_ms": vr.search_ms, "states_per_s": vs,
+            line["variants"][names[int(vr.variant)]] = {"search_ms": vr.search_ms, "states_per_s": vs,
                                            "nominal_roofline_frac": vs * (n + 1) / peak,
                                            "same_argmin": int(vr.argmin_bits) == int(r.argmin_bits)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

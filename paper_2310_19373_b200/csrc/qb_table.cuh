@@ -67,9 +67,9 @@ __device__ __forceinline__ void outer_flip(const TableParams& p, int ell, float 
     if (ell == ELL) {
       V += (long long)(sg * (p.d[ELL] + F[ELL - B]));
 #pragma unroll
-      for (int i = 0; i < B; ++i) H[i] = fmaf(sg, p.Qs[i][ELL], H[i]);
+      for (int i = 0; i < B; ++i) H[i] = fmaf(sg, p.Qs[ELL][i], H[i]);  // row ELL (Qs symmetric): vector loads
 #pragma unroll
-      for (int m = 0; m < L - B; ++m) F[m] = fmaf(sg, p.Qs[B + m][ELL], F[m]);
+      for (int m = 0; m < L - B; ++m) F[m] = fmaf(sg, p.Qs[ELL][B + m], F[m]);
     } else {
       outer_flip<B, L, ELL + 1>(p, ell, sg, V, H, F);
     }

@@ -9,6 +9,10 @@
 #include <vector>
 #include "../paper_2310_19373_b200/csrc/qb_tc_ptx.cuh"
 
+__host__ __device__ constexpr uint32_t off32(int r, int k) {
+  return (uint32_t)((r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
 using namespace qb::tc;
 
 template <int N, bool F16ACC>
@@ -51,6 +55,43 @@ __global__ void mma_test(const uint16_t* A, const uint16_t* B, uint32_t* out_raw
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<(N < 32 ? 32 : N)>(taddr);
+}
+
+
+// K = 32 (two kind::f16 K-steps), fp32 accumulators, the operand layout of qb_tc.cuh
+__global__ void mma_k32(const uint16_t* A, const uint16_t* B, uint32_t* out) {
+  __shared__ __align__(1024) uint8_t sA[128 * 64];
+  __shared__ __align__(1024) uint8_t sB[128 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, warp = t >> 5;
+  for (int k = 0; k < 32; ++k) {
+    *reinterpret_cast<uint16_t*>(sA + off32(t, k)) = A[t * 32 + k];
+    *reinterpret_cast<uint16_t*>(sB + off32(t, k)) = B[t * 32 + k];
+  }
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<128>(&tbase);
+  if (t == 0) mbar_init(&bar, 1);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (t == 0) {
+    const uint64_t ad = smem_desc(smem_u32(sA), 128, 512), bd = smem_desc(smem_u32(sB), 128, 512);
+    mma_f16(tbase, ad, bd, idesc_f16_f32(128, 128), 0);
+    mma_f16(tbase, ad + 16, bd + 16, idesc_f16_f32(128, 128), 1);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c = 0; c < 128; c += 32) {
+    uint32_t r[32];
+    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 32; ++i) out[t * 128 + c + i] = r[i];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<128>(tbase);
 }
 
 static float u2f(uint32_t u) {
@@ -121,12 +162,69 @@ static int run(int range) {
   return bad_raw + bad_pack ? 1 : 0;
 }
 
+
+// the qb_tc.cuh pair encoding with random fields (hc in [-100, 100], Tc' and O anywhere in their
+// ranges): every TMEM cell must equal the exact integer dot product bit for bit
+static int run_pairs(int seed) {
+  srand(seed);
+  std::vector<uint16_t> A(128 * 32, 0), B(128 * 32, 0);
+  std::vector<long long> Ai(128 * 32, 0), Bi(128 * 32, 0);
+  auto setA = [&](int r, int k, long long v) { Ai[r * 32 + k] = v; A[r * 32 + k] = h((float)v); };
+  auto setB = [&](int r, int k, long long v) { Bi[r * 32 + k] = v; B[r * 32 + k] = h((float)v); };
+  for (int r = 0; r < 128; ++r) {
+    const int O = rand() % 1025;
+    for (int i = 0; i < 10; ++i) {
+      const int hc = rand() % 201 - 100;
+      setA(r, i, hc);
+      setA(r, 16 + i, hc);
+    }
+    setA(r, 10, 1); setA(r, 11, O); setA(r, 12, 2048);
+    setA(r, 26, 2048); setA(r, 27, O);
+  }
+  for (int p = 0; p < 128; ++p) {
+    const int zl = (p * 37 + seed) & 511, zh = zl + 512;
+    for (int i = 0; i < 10; ++i) {
+      setB(p, i, (zl >> i) & 1);
+      setB(p, 16 + i, 2048 * ((zh >> i) & 1));
+    }
+    setB(p, 10, rand() % 1024); setB(p, 11, 1); setB(p, 12, 4096);
+    setB(p, 26, rand() % 1024); setB(p, 27, 2048);
+  }
+  uint16_t *dA, *dB;
+  uint32_t* d;
+  cudaMalloc(&dA, A.size() * 2);
+  cudaMalloc(&dB, B.size() * 2);
+  cudaMalloc(&d, 128 * 128 * 4);
+  cudaMemcpy(dA, A.data(), A.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 2, cudaMemcpyHostToDevice);
+  mma_k32<<<1, 128>>>(dA, dB, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<uint32_t> out(128 * 128);
+  cudaMemcpy(out.data(), d, out.size() * 4, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  for (int m = 0; m < 128; ++m)
+    for (int n = 0; n < 128; ++n) {
+      long long ref = 0;
+      for (int k = 0; k < 32; ++k) ref += Ai[m * 32 + k] * Bi[n * 32 + k];
+      if ((double)u2f(out[m * 128 + n]) != (double)ref) {
+        if (bad < 4) printf("  k32 mismatch m=%d n=%d ref=%lld got=%.1f\n", m, n, ref, u2f(out[m * 128 + n]));
+        ++bad;
+      }
+    }
+  printf("K=32 pair encoding seed %d: %s, %d mismatches\n", seed, e == cudaSuccess ? "ok" : cudaGetErrorString(e), bad);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(d);
+  return bad ? 1 : 0;
+}
+
 int main() {
   int bad = 0;
   bad |= run<128, false>(8);
   bad |= run<128, true>(8);
   bad |= run<256, true>(8);
   bad |= run<64, true>(3);
+  for (int sd = 1; sd <= 8; ++sd) bad |= run_pairs(sd);
   printf(bad ? "FAIL\n" : "ALL OK\n");
   return bad;
 }
