@@ -47,7 +47,7 @@ ALU_PEAKS = os.path.join(ROOT, "profiles", "r01_alu_peaks.json")
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
 # ncu --set full capture of the search kernel (DRAM bytes per launch, n=40 config E)
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r04_ncu_search_summary.txt")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r05_ncu_search_summary.txt")
 
 
 def ncu_traffic_bytes():
@@ -67,7 +67,7 @@ def ncu_traffic_bytes():
 
 
 # SASS instructions per state of the table kernel's inner block (cuobjdump count)
-SASS_INSTR_PER_STATE = 1.09  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r04_ncu_search_summary.txt)
+SASS_INSTR_PER_STATE = 1.08  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r05_ncu_search_summary.txt)
 
 
 def parse():
@@ -356,10 +356,10 @@ def main():
     roofline = {
         "bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
         "frac": achieved / peak, "traffic": ncu_traffic_bytes(),
-        "traffic_note": "DRAM bytes per search launch from the committed ncu capture (profiles/r04_ncu_search_summary.txt, "
+        "traffic_note": f"DRAM bytes per search launch from the committed ncu capture ({os.path.relpath(NCU_SUMMARY, ROOT)}, "
                         "n=40): the per-chunk minima and CTA records; the algorithmic HBM traffic per state is 0",
         "basis": f"nominal {n + 1} ops/state (SURVEY.md §8d: n-1 field adds + 1 value add + 1 min) vs the "
-                 f"{peak_src}; the table kernel issues ~{SASS_INSTR_PER_STATE} SASS instr/state, so frac > 1 "
+                 f"{peak_src}; the coarse kernel issues ~{SASS_INSTR_PER_STATE} SASS instr/state, so frac > 1 "
                  "measures the algorithmic saving and issue_frac (vs 4 warp-instr/SM/clk) the kernel quality",
         "issue_frac": per_launch_states * SASS_INSTR_PER_STATE / search_s / issue_peak,
         "search_ms_per_launch": search_s * 1e3,
