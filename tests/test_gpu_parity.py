@@ -418,6 +418,20 @@ def test_adversarial_value_ranges_tc_kernel(kind):
         assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key), (kind, args)
 
 
+def test_tc_kernel_sharded_partial_rounds():
+    """Shards whose chunk counts are not multiples of the 128-row MMA (inactive rows in the last
+    round) combine to the unsharded answer through the tensor-core pass."""
+    for name in ("E", "D"):
+        c = instances.config_coeffs(name, 3, n=34)
+        whole = _lib.solve(c, variant=_lib.VARIANT_TABLE)
+        for S in (3, 7):
+            parts = [_lib.solve(c, shard=i, shard_count=S, variant=_lib.VARIANT_TC) for i in range(S)]
+            assert all(p.variant == _lib.VARIANT_TC for p in parts)
+            best = min(parts, key=lambda r: (r.value_key, r.tie_key))
+            assert (best.argmin_bits, best.value, best.tie_key) == (whole.argmin_bits, whole.value, whole.tie_key)
+            assert sum(p.states for p in parts) == 1 << 34
+
+
 def test_tc_kernel_n40():
     """n=40 (config E) through the tensor-core pass: same answer as the default coarse kernel."""
     c = instances.config_coeffs("E", 0)
