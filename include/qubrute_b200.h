@@ -95,6 +95,15 @@ double qb_eval_upper(const double* coeffs, int n, const double* x);
 int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule,
              uint32_t shard, uint32_t shard_count, int variant, qb_result* out);
 
+/* The same solve sharded over several GPUs from one process (qb_solve with
+ * num_gpus): shard i of ndev runs on devices[i] in its own host thread, and the shard results are
+ * combined on the host by the lexicographic minimum of (value_key, tie_key), which is the reference's
+ * tie rule (combine_subspace_minima, solver.py:173-185).  states / launches / grid / candidates
+ * are summed, kernel_ms / search_ms are the maximum over shards.  A device may appear more than
+ * once (its shards then run one after another). */
+int qb_solve_devices(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule,
+                     const int* devices, int ndev, int variant, qb_result* out);
+
 /* Every minimiser of the subspace {x : x >> (n - m_fix) == suffix} (BASELINE config A: "min
  * value + all minimising vectors"; the reference returns one, SPEC.md:273 lists this as a
  * non-goal).  Sorted by the Gray tie rule m_tie, so out[0] is what qb_solve returns.  Writes up

@@ -86,6 +86,9 @@ SIGNATURES = {
     "qb_eval_upper": (ctypes.c_double, [_dp, ctypes.c_int, _dp]),
     "qb_solve": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(QbResult)]),
+    "qb_solve_devices": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(QbResult)]),
     "qb_all_minimisers": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _u64p,
                                          ctypes.c_uint64, _u64p, _dp]),
     "qb_gray_scan": (ctypes.c_int, [_dp, _dp, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _dp,
@@ -205,6 +208,18 @@ def solve(coeffs, m_fix: int = 0, suffix: int = 0, m_tie: int = 0, tie_rule: int
     rc = lib().qb_solve(_ptr(c), c.shape[0], m_fix, suffix, m_tie, tie_rule, shard, shard_count, variant,
                         ctypes.byref(out))
     check(rc, "qb_solve")
+    return out
+
+
+def solve_devices(coeffs, devices, m_fix: int = 0, suffix: int = 0, m_tie: int = 0, tie_rule: int = TIE_GRAY,
+                  variant: int = VARIANT_AUTO) -> QbResult:
+    """One solve sharded over several GPUs of this process (qb_solve_devices): shard i on devices[i]."""
+    c = _f64(coeffs)
+    devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+    out = QbResult()
+    rc = lib().qb_solve_devices(_ptr(c), c.shape[0], m_fix, suffix, m_tie, tie_rule, devs, len(devices), variant,
+                                ctypes.byref(out))
+    check(rc, "qb_solve_devices")
     return out
 
 

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -835,6 +836,60 @@ double qb_eval_upper(const double* coeffs, int n, const double* x) { return qb::
 int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule, uint32_t shard,
              uint32_t shard_count, int variant, qb_result* out) {
   return qb::solve_impl(coeffs, n, m_fix, suffix, m_tie, tie_rule, shard, shard_count, variant, out);
+}
+
+int qb_solve_devices(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule,
+                     const int* devices, int ndev, int variant, qb_result* out) {
+  if (!devices || !out) return qb::fail(QB_E_ARG, "null pointer");
+  if (ndev < 1 || ndev > 64) return qb::fail(QB_E_ARG, "ndev must be in [1, 64]");
+  int c = 0;
+  qb_device_count(&c);
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= c) return qb::fail(QB_E_ARG, "device index out of range");
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<qb_result> parts((size_t)ndev);
+  std::vector<int> rcs((size_t)ndev, QB_OK);
+  std::vector<std::string> errs((size_t)ndev);
+  std::vector<std::thread> pool;
+  for (int i = 0; i < ndev; ++i)
+    pool.emplace_back([&, i] {
+      rcs[i] = qb_init(devices[i]);
+      if (rcs[i] == QB_OK)
+        rcs[i] = qb::solve_impl(coeffs, n, m_fix, suffix, m_tie, tie_rule, (uint32_t)i, (uint32_t)ndev, variant,
+                                &parts[i]);
+      if (rcs[i] != QB_OK) errs[i] = qb_last_error();
+    });
+  for (auto& t : pool) t.join();
+  for (int i = 0; i < ndev; ++i)
+    if (rcs[i] != QB_OK) return qb::fail(rcs[i], "shard " + std::to_string(i) + ": " + errs[i]);
+  int w = -1;
+  for (int i = 0; i < ndev; ++i) {
+    if (parts[i].states == 0) continue;
+    if (w < 0 || parts[i].value_key < parts[w].value_key ||
+        (parts[i].value_key == parts[w].value_key && parts[i].tie_key < parts[w].tie_key))
+      w = i;
+  }
+  if (w < 0) return qb::fail(QB_E_INTERNAL, "no shard scanned any state");
+  qb_result r = parts[w];
+  r.states = 0;
+  r.candidates = 0;
+  r.launches = 0;
+  r.grid = 0;
+  r.kernel_ms = r.search_ms = r.collect_ms = 0.0;
+  r.exact = 1;
+  for (int i = 0; i < ndev; ++i) {
+    r.states += parts[i].states;
+    r.candidates += parts[i].candidates;
+    r.launches += parts[i].launches;
+    r.grid += parts[i].grid;
+    r.kernel_ms = std::max(r.kernel_ms, parts[i].kernel_ms);
+    r.search_ms = std::max(r.search_ms, parts[i].search_ms);
+    r.collect_ms = std::max(r.collect_ms, parts[i].collect_ms);
+    r.exact &= parts[i].exact;
+  }
+  r.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *out = r;
+  return QB_OK;
 }
 
 int qb_all_minimisers(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, uint64_t* out,

@@ -54,6 +54,9 @@ def test_no_silent_cpu_fallback_without_gpu(cuda_available):
         pytest.skip("GPU present")
     with pytest.raises(qb.BackendError):
         qb.solve_incremental(qb.QuboInstance(np.eye(4)))
+    # the multi-device entry point fails loudly too (no device to shard over)
+    with pytest.raises((qb.BackendError, ValueError)):
+        _lib.solve_devices(np.eye(4), [0, 1])
 
 
 def test_version_string():

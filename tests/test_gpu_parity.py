@@ -140,6 +140,21 @@ def test_sharding_is_invariant():
             assert sum(p.states for p in parts) == 1 << n
 
 
+def test_solve_devices_matches_single_solve():
+    """qb_solve_devices (one process, shard i on devices[i], host combine) == one launch; with the one
+    GPU here every shard runs on device 0 (the same code path a multi-GPU box runs in parallel)."""
+    for name, n in (("D", 30), ("E", 32), ("A", 20)):
+        c = instances.config_coeffs(name, 2, n=n)
+        whole = _lib.solve(c)
+        for ndev in (1, 2, 3):
+            r = _lib.solve_devices(c, [0] * ndev)
+            assert (r.argmin_bits, r.value, r.tie_key) == (whole.argmin_bits, whole.value, whole.tie_key)
+            assert r.states == 1 << n
+        r = _lib.solve_devices(c, [0, 0], m_fix=3, suffix=5, m_tie=3)
+        w = _lib.solve(c, 3, 5, 3)
+        assert (r.argmin_bits, r.value, r.tie_key) == (w.argmin_bits, w.value, w.tie_key)
+
+
 def test_config_e_n40_properties():
     """n=40 is beyond the oracle: check the argmin against exact CPU scans of the
     subspace that contains it and of random other subspaces; the default (coarse-filter)
