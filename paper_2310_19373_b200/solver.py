@@ -22,7 +22,7 @@ from __future__ import annotations
 
 import time
 from dataclasses import dataclass
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -70,11 +70,14 @@ class SubspaceSpec:
 @dataclass(frozen=True)
 class SolveConfig:
     """Solver knobs (solver.py:82-96).  ``threads`` only selects the default ``fixed_bits``
-    (and hence the tie rule), exactly as in the reference; the GPU does the scanning."""
+    (and hence the tie rule), exactly as in the reference; the GPU does the scanning.
+    ``devices`` (extension, SURVEY.md section 5 "Config / flags"): CUDA devices of this process
+    to shard the solve over (qb_solve_devices); None = the current device."""
 
     threads: int = 1
     fixed_bits: Optional[int] = None
     mode: str = "incremental"
+    devices: Optional[Tuple[int, ...]] = None
 
     def __post_init__(self) -> None:
         if self.threads < 1:
@@ -83,6 +86,20 @@ class SolveConfig:
             raise ValueError(f"fixed_bits must be >= 0, got {self.fixed_bits}")
         if self.mode not in MODES:
             raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.devices is not None:
+            devs = tuple(self.devices)
+            if not devs or any((not isinstance(d, (int, np.integer))) or d < 0 for d in devs):
+                raise ValueError(f"devices must be a non-empty sequence of device indices, got {self.devices!r}")
+            object.__setattr__(self, "devices", tuple(int(d) for d in devs))
+
+
+def _gpu_solve(coeffs, m_fix: int, suffix: int, m_tie: int, rule: int, devices=None):
+    """One solve on the current device, or sharded over ``devices`` (one shard per entry)."""
+    if devices is None:
+        return _lib.solve(coeffs, m_fix, suffix, m_tie, rule)
+    if len(devices) == 1:
+        return _lib.solve(coeffs, m_fix, suffix, m_tie, rule, device=devices[0])
+    return _lib.solve_devices(coeffs, devices, m_fix, suffix, m_tie, rule)
 
 
 def _solution(inst: QuboInstance, res, evaluations: int, t0: float) -> Solution:
@@ -106,12 +123,15 @@ def solve_naive(instance: QuboInstance, *, max_n: int = NAIVE_MAX_DIM) -> Soluti
     return _solution(instance, res, (1 << instance.n) - 1, t0)
 
 
-def solve_incremental(instance: QuboInstance) -> Solution:
-    """Exhaustive Gray-code solve; ties to the lowest global Gray rank (solver.py:118-136)."""
+def solve_incremental(instance: QuboInstance, *, devices=None) -> Solution:
+    """Exhaustive Gray-code solve; ties to the lowest global Gray rank (solver.py:118-136).
+    ``devices``: optional CUDA devices to shard over (extension; see SolveConfig)."""
     if instance.n > MAX_DIM:
         raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+    if devices is not None:
+        devices = SolveConfig(devices=devices).devices
     t0 = time.perf_counter()
-    res = _lib.solve(instance.coeffs, 0, 0, 0, _lib.TIE_GRAY)
+    res = _gpu_solve(instance.coeffs, 0, 0, 0, _lib.TIE_GRAY, devices)
     return _solution(instance, res, (1 << instance.n) - 1, t0)
 
 
@@ -161,7 +181,7 @@ def solve_parallel(instance: QuboInstance, config: SolveConfig | None = None) ->
     """All 2^m subspaces in one GPU launch, lowest-suffix tie rule (solver.py:193-229)."""
     m = _resolve_m(instance, config)
     t0 = time.perf_counter()
-    res = _lib.solve(instance.coeffs, 0, 0, m, _lib.TIE_GRAY)
+    res = _gpu_solve(instance.coeffs, 0, 0, m, _lib.TIE_GRAY, config.devices if config is not None else None)
     return _solution(instance, res, (1 << instance.n) - (1 << m), t0)
 
 
@@ -235,5 +255,5 @@ def solve(instance: QuboInstance, config: SolveConfig | None = None) -> Solution
     if config.mode == "naive":
         return solve_naive(instance)
     if config.mode == "incremental":
-        return solve_incremental(instance)
+        return solve_incremental(instance, devices=config.devices)
     return solve_parallel(instance, config)

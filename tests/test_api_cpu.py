@@ -74,3 +74,12 @@ def test_delta_and_split_consistency():
         x[l] ^= 1
         v += qb.delta(form, x, l)
         assert abs(v - qb.evaluate(inst, x)) <= 1e-9
+
+
+def test_solve_config_devices_validation():
+    # extension knob: devices to shard over, validated like the reference's knobs
+    assert qb.SolveConfig(devices=[0, 1]).devices == (0, 1)
+    assert qb.SolveConfig().devices is None
+    for bad in ([], [-1], ["0"]):
+        with pytest.raises(ValueError):
+            qb.SolveConfig(devices=bad)

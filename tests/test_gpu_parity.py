@@ -155,6 +155,20 @@ def test_solve_devices_matches_single_solve():
         assert (r.argmin_bits, r.value, r.tie_key) == (w.argmin_bits, w.value, w.tie_key)
 
 
+def test_solver_devices_knob():
+    """SolveConfig(devices=...) / solve_incremental(devices=...) shard through qb_solve_devices and
+    return the reference's answer (all shards on device 0 here)."""
+    c = instances.config_coeffs("D", 4, n=26)
+    inst = qb.QuboInstance(c)
+    ref_inc = qb.solve_incremental(inst)
+    ref_par = qb.solve_parallel(inst, qb.SolveConfig(threads=8))
+    got_inc = qb.solve_incremental(inst, devices=(0, 0, 0))
+    got_par = qb.solve_parallel(inst, qb.SolveConfig(threads=8, devices=(0, 0)))
+    got_dsp = qb.solve(inst, qb.SolveConfig(mode="incremental", devices=(0,)))
+    for a, b in ((ref_inc, got_inc), (ref_par, got_par), (ref_inc, got_dsp)):
+        assert _bits(a) == _bits(b) and a.value == b.value and a.evaluations == b.evaluations
+
+
 def test_config_e_n40_properties():
     """n=40 is beyond the oracle: check the argmin against exact CPU scans of the
     subspace that contains it and of random other subspaces; the default (coarse-filter)
