@@ -31,12 +31,6 @@
 // TMEM: two 128-column tile buffers per CTA, two CTAs per SM (all 512 columns).
 #pragma once
 #include <cuda_fp16.h>
-#ifdef QB_TC_TRACE
-#include <cstdio>
-#define QB_TR(...) __VA_ARGS__
-#else
-#define QB_TR(...)
-#endif
 #include "qb_coarse.cuh"
 #include "qb_tc_ptx.cuh"
 
@@ -180,33 +174,25 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
       const uint64_t zdesc = tc::smem_desc(tc::smem_u32(zmat), tc::kLBO, tc::kSBO);
       const uint64_t adesc[2] = {tc::smem_desc(tc::smem_u32(a_tile[0]), tc::kLBO, tc::kSBO),
                                  tc::smem_desc(tc::smem_u32(a_tile[1]), tc::kLBO, tc::kSBO)};
-      QB_TR(long long ta = 0, te = 0, ti = 0; uint32_t ng = 0;)
       for (uint32_t g = 0;; ++g) {
         const int s = g & 1;
-        QB_TR(long long c0 = clock64();)
         tc::mbar_wait(&bar_a[s], (g >> 1) & 1);
-        QB_TR(ta += clock64() - c0; ++ng;)
         if (*(volatile int*)&stop_flag[s]) break;
         tc::tc_fence_after();
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          QB_TR(long long c1 = clock64();)
           if (g > 0 || t >= 2) {
             tc::mbar_wait(&bar_empty[t & 1], ((t >> 1) + 1) & 1);
             tc::tc_fence_after();
           }
-          QB_TR(long long c2 = clock64(); te += c2 - c1;)
           // Z cell rows [128 t, 128 t + 128): 16 8-row groups of 512 B; descriptor addresses in 16 B units
           const uint64_t zd = zdesc + (uint64_t)(t * TC_TILE_N * TC_K * 2 / 16);
           const uint32_t d = tmem + (t & 1) * TC_TILE_N;
           tc::mma_f16(d, adesc[s], zd, idesc, 0u);
           tc::mma_f16(d, adesc[s] + tc::kKStep / 16, zd + tc::kKStep / 16, idesc, 1u);
           tc::mma_commit(&bar_full[t & 1]);
-          QB_TR(ti += clock64() - c2;)
         }
       }
-      QB_TR(if (blockIdx.x == 0) printf("issuer: batches %u, per batch: wait_a %.0f wait_empty %.0f issue %.0f clk\n", ng,
-                                      (double)ta / ng, (double)te / ng, (double)ti / ng);)
     }
     __syncwarp();
   } else {
@@ -248,17 +234,12 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
       }
       return true;
     };
-    QB_TR(long long tq0 = 0, tq1 = 0, tq2 = 0;)
     auto publish = [&](int slot) {
-      QB_TR(long long q0 = clock64();)
       ld_next = tc_ld(lim, V, p.tc_shift, p.tc_bias);
       tc_write_row<B>(a_tile[slot], tid, H, p.tc_scale, (float)(1023 - ld_next), active);
-      QB_TR(long long q1 = clock64(); tq0 += q1 - q0;)
       tc::fence_async_smem();
-      QB_TR(long long q2 = clock64(); tq1 += q2 - q1;)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bar_a[slot]);
-      QB_TR(tq2 += clock64() - q2;)
     };
     auto publish_stop = [&](int slot) {  // no batch g: the issuer leaves its loop
       if (tid == 0) stop_flag[slot] = 1;
@@ -269,9 +250,7 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
     bool more = fetch_round();
     if (more) publish(0);
     else publish_stop(0);
-    QB_TR(long long tp = 0, tw = 0, tl = 0, tn = 0, tr = 0, tstart = clock64(); uint32_t nb = 0;)
     for (uint32_t g = 0; more; ++g) {
-      QB_TR(long long d0 = clock64(); ++nb;)
       // the block consumed in this iteration
       const bool cur_active = active;
       const unsigned long long cur_c = c, cur_ci = ci, cur_key_hi = key_hi;
@@ -290,11 +269,8 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int b = t & 1;
-        QB_TR(long long e0 = clock64();)
         tc::mbar_wait(&bar_full[b], (t >> 1) & 1);
         tc::tc_fence_after();
-        QB_TR(tw += clock64() - e0;)
-        QB_TR(long long e1 = clock64();)
         // the whole tile into registers, then hand the buffer back before folding it
         uint32_t r[TC_TILE_N];
 #pragma unroll
@@ -304,14 +280,11 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bar_empty[b]);
-        QB_TR(long long e2 = clock64(); tl += e2 - e1;)
 #pragma unroll
         for (int i = 0; i < TC_TILE_N; i += 16)
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc[k] &= r[i + 2 * k] & r[i + 2 * k + 1];
-        QB_TR(tn += clock64() - e2;)
         if (t == 1) {  // A rows of the next block: needed once tile 2 has drained buffer 0
-          QB_TR(long long d0b = clock64();)
           // prepare the next block (outer Gray flip, or the next round's chunks) while the tensor core
           // works on this one
           if (j + 1 < (1u << LO)) {
@@ -326,10 +299,8 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
           }
           if (more) publish((g + 1) & 1);
           else publish_stop((g + 1) & 1);
-          QB_TR(tp += clock64() - d0b;)
         }
       }
-      QB_TR(long long d2 = clock64();)
       if (!cur_active) continue;
       const uint32_t all = (acc[0] & acc[1] & acc[2]) & (acc[3] & acc[4] & acc[5]) & (acc[6] & acc[7]);
       const bool pass = (all & 0x200400u) != 0x200400u;
@@ -352,10 +323,7 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
         if (skip_min != LLONG_MAX) cmin = min(cmin, skip_min - slack);
         if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[cur_ci] = cmin;
       }
-      QB_TR(tr += clock64() - d2;)
     }
-    QB_TR(if (blockIdx.x == 0 && (tid & 31) == 0) printf("warp %d: batches %u, per batch: row %.0f fence %.0f arrive %.0f prepare %.0f wait_full %.0f ld %.0f and %.0f tail %.0f total %.0f clk\n", warp, nb, (double)tq0 / nb, (double)tq1 / nb, (double)tq2 / nb,
-                                        (double)tp / nb, (double)tw / nb, (double)tl / nb, (double)tn / nb, (double)tr / nb, (double)(clock64() - tstart) / nb);)
   }
   tc::tc_fence_before();
   __syncthreads();
