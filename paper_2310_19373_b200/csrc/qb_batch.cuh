@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   __shared__ float sQ[BATCH_NMAX][BATCH_NMAX + 1];   // quantized: diagonal on the diagonal, symmetric off
   __shared__ __align__(16) float sT[NT];
   __shared__ double sred[BATCH_TPB_MAX / 32];
-  __shared__ int sflag[2];                           // [0]: not integral, [1]: not exact
+  __shared__ int sflag[3];                           // [0]: not integral, [1]: not exact, [2]: not finite
   __shared__ unsigned long long scand[BATCH_CAP];
   __shared__ unsigned int schunk[CHUNK_CAP];
   __shared__ int scount, schunks;
@@ -107,15 +107,22 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   const int lane = tid & 31, warp = tid >> 5;
 
   // ---- 0. fold (QuboInstance convention, core.py:66-72) into shared memory: one pass over global
-  if (tid == 0) { sflag[0] = sflag[1] = 0; scount = 0; schunks = 0; }
+  if (tid == 0) { sflag[0] = sflag[1] = sflag[2] = 0; scount = 0; schunks = 0; }
+  __syncthreads();
   for (int idx = tid; idx < n * n; idx += nth) {
     const int i = idx / n, j = idx % n;
     if (j < i) continue;
-    const double v = (i == j) ? C[idx] : __dadd_rn(C[idx], C[j * n + i]);
+    const double a = C[idx], b = (i == j) ? 0.0 : C[j * n + i];
+    if (!isfinite(a) || !isfinite(b)) sflag[2] = 1;  // reported to the host as QB_E_ARG
+    const double v = (i == j) ? a : __dadd_rn(a, b);
     sC[i][j] = v;
     sC[j][i] = v;
   }
   __syncthreads();
+  if (sflag[2]) {  // every coefficient is read here, so the host needs no pass over the batch
+    if (tid == 0) bp.out[blockIdx.x] = BatchOut{0ull, 0.0, 3, 0};
+    return;
+  }
 
   // ---- 1. quantization: bound M = max(r_in, max row abs sum), as in qb_api.cu quantize()
   double part_rin = 0.0, part_row = 0.0;

@@ -10,7 +10,7 @@ constexpr int BATCH_TPB_MAX = 256;
 struct BatchOut {
   unsigned long long x;  // argmin bits
   double value;          // eval_upper(argmin)
-  int status;            // 0 ok, 1 candidate overflow (host fallback), 2 no candidate (bug)
+  int status;            // 0 ok, 1 candidate overflow (host fallback), 2 no candidate (bug), 3 non-finite input
   int candidates;
 };
 

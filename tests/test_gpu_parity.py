@@ -202,6 +202,19 @@ def test_batch_config_c_golden(golden):
     assert [_bits(s) for s in sols] == cb["bits"][:64]
 
 
+def test_batch_rejects_non_finite():
+    """Non-finite coefficients anywhere in a batch (also below the diagonal) raise ValueError like
+    QuboInstance does; the check runs in the batch kernel (no host pass over the batch)."""
+    batch = instances.config_batch(64, 16)
+    for pos in ((5, 3, 7), (63, 9, 2), (0, 0, 0)):
+        bad = batch.copy()
+        bad[pos] = np.nan if pos != (0, 0, 0) else np.inf
+        with pytest.raises(ValueError, match="finite"):
+            qb.solve_batch(bad)
+    bits, vals, _ = _lib.solve_batch(batch)  # and the device is fine afterwards
+    assert len(bits) == 64
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 9, 10, 11, 13, 16, 20])
 def test_batch_ties_and_sizes(n):
     count = 40
