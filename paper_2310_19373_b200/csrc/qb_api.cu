@@ -195,7 +195,7 @@ static double sym(const double* c, int n, int i, int j) {
 
 // Integer scaling: q = rint(c * 2^e) with every partial sum the device forms below 2^24.
 // BE: block bits (their relative values are formed in fp32); B: table bits (T is built over them).
-static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
+static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false) {
   const double LIM = 16777215.0;  // 2^24 - 1
   auto bound = [&](auto get) {
     double r_in = 0.0, rmax = 0.0;
@@ -296,7 +296,8 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl) {
   // coarse image for the tensor-core pass (qb_tc.cuh): D(z) = sum_i z_i hc_i + Tc(z) + beta must lie
   // in [0, 1023] (11-bit fields of the fp32 accumulators, f16-exact operands).  With
   // R_H = sum_{i<B} sum_{q>=B} |q_iq| (bound on sum |H_i|), Hc = R_H 2^-s + B/2 bounds sum |hc_i|, and
-  // beta = ceil(Hc) - min Tc: D lies in [0, 2 Hc + 1 + Tc span].
+  // beta = ceil(Hc) - min Tc: D lies in [0, 2 Hc + 1 + Tc span].  Only built for that kernel.
+  if (!tc_image) return QB_OK;
   double r_h = 0.0, tmin = 0.0, tmax = 0.0;
   for (int i = 0; i < B && i < n; ++i)
     for (int q2 = B; q2 < n; ++q2) r_h += std::fabs(i < q2 ? q[(size_t)i * n + q2] : q[(size_t)q2 * n + i]);
@@ -433,7 +434,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
                       (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC ||
                        (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   QB_TMARK("geometry");
-  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl)) return rc;
+  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc)) return rc;
   QB_TMARK("quantize");
 
   TableParams& P = *pl.P;
