@@ -474,9 +474,11 @@ def test_tc_kernel_sharded_partial_rounds():
             assert sum(p.states for p in parts) == 1 << 34
 
 
-def test_tc_kernel_n40():
-    """n=40 (config E) through the tensor-core pass: same answer as the default coarse kernel."""
-    c = instances.config_coeffs("E", 0)
+@pytest.mark.parametrize("name", ["E", "D", "B"])
+def test_tc_kernel_n40(name):
+    """n=40 through the tensor-core pass (sparse fp32, dense int +-1000, dense fp32): same answer as
+    the default coarse kernel."""
+    c = instances.config_coeffs(name, 0, n=40)
     a = _lib.solve(c)
     b = _lib.solve(c, variant=_lib.VARIANT_TC)
     assert b.variant == _lib.VARIANT_TC
