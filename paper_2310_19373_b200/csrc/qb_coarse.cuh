@@ -26,6 +26,9 @@ namespace qb {
 // (LDCU.128 = 8 states, broadcast through the operand path, not replicated per lane), and
 // VIMNMX3.U16x2 folds two candidate pairs into the running pair-minimum (4 states per min).
 constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw and Tc components
+#ifndef QB_LDC_MASK
+#define QB_LDC_MASK 0x8080  // table rows u (bit u) taking the per-lane LDC + VIADDMNMX path (measured)
+#endif
 #ifndef QB_EXACT_NOINLINE
 #define QB_EXACT_NOINLINE 1  // long chunks call the exact re-evaluation out of line (measured n=40: 52 -> 41 ms)
 #endif
@@ -87,6 +90,23 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       unsigned acc2 = 0u;
+      if constexpr (QB_LDC_MASK != 0) {
+        if ((QB_LDC_MASK >> (u + h)) & 1) {
+          // per-lane table loads (LDC) feeding fused add+min (VIADDMNMX.U16x2, GPR operands only):
+          // fewer issue slots per state than the uniform path, at the cost of the ALU pipe
+          unsigned a0 = 0xffffffffu, a1 = 0xffffffffu;
+#pragma unroll
+          for (int m = 0; m < NP; m += 4) {
+            const uint4 t = *reinterpret_cast<const uint4*>(&p.Tc2[(u + h) * NP + m]);
+            a0 = __viaddmin_u16x2(Bw2[m], t.x, a0);
+            a1 = __viaddmin_u16x2(Bw2[m + 1], t.y, a1);
+            a0 = __viaddmin_u16x2(Bw2[m + 2], t.z, a0);
+            a1 = __viaddmin_u16x2(Bw2[m + 3], t.w, a1);
+          }
+          r2[h] = umin2(a0, a1) + A2[u + h];
+          continue;
+        }
+      }
 #pragma unroll
       for (int m = 0; m < NP; m += 4) {
         const uint4 t = *reinterpret_cast<const uint4*>(&p.Tc2[(u + h) * NP + m]);
