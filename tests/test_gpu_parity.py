@@ -192,6 +192,22 @@ def test_config_e_n40_properties():
         assert v >= sol.value
 
 
+@pytest.mark.parametrize("rep", [1, 2, 3])
+def test_config_e_n40_other_seeds(rep):
+    """Config E at n=40 for further seeds: coarse kernel (with its LDC rows), fp32 table kernel and
+    tensor-core pass agree, and the argmin is the exact minimum of its own 2^23-state subspace."""
+    c = instances.config_coeffs("E", rep)
+    auto = _lib.solve(c)
+    table = _lib.solve(c, variant=_lib.VARIANT_TABLE)
+    tcr = _lib.solve(c, variant=_lib.VARIANT_TC)
+    for r in (table, tcr):
+        assert (auto.argmin_bits, auto.value, auto.tie_key) == (r.argmin_bits, r.value, r.tie_key)
+    x = int(auto.argmin_bits)
+    m = 17
+    bits, val, _ = O.solve_subspaces(c, m, x >> (40 - m), (x >> (40 - m)) + 1, threads=8)
+    assert bits == x and val == auto.value
+
+
 def test_batch_config_c_golden(golden):
     cb = golden["configC"]
     batch = instances.config_batch(cb["count"], cb["n"])
