@@ -27,7 +27,7 @@ namespace qb {
 // VIMNMX3.U16x2 folds two candidate pairs into the running pair-minimum (4 states per min).
 constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw and Tc components
 #ifndef QB_LDC_MASK
-#define QB_LDC_MASK 0x8080  // table rows u (bit u) taking the per-lane LDC + VIADDMNMX path (measured)
+#define QB_LDC_MASK 0x4040  // table rows u (bit u) taking the per-lane LDC + VIADDMNMX path (measured)
 #endif
 #ifndef QB_EXACT_NOINLINE
 #define QB_EXACT_NOINLINE 1  // long chunks call the exact re-evaluation out of line (measured n=40: 52 -> 41 ms)
