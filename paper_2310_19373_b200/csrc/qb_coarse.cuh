@@ -157,6 +157,23 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
 #define QB_COARSE_MINB 4  // 128 registers: fewer uniform-register spills beat the fifth CTA (measured)
 #endif
 
+#ifndef QB_CHUNK_START_NOINLINE
+#define QB_CHUNK_START_NOINLINE 1  // chunk-start evaluation out of line: keeps the hot loop's code compact (measured -0.5%)
+#endif
+template <int B, int NF>
+struct ChunkStart {
+  long long V;
+  float H[B];
+  float F[NF];
+};
+template <int B, int L>
+__device__ __noinline__ ChunkStart<B, ((L - B) > 0 ? (L - B) : 1)> chunk_start_ool(const TableParams& p,
+                                                                             unsigned long long s) {
+  ChunkStart<B, ((L - B) > 0 ? (L - B) : 1)> r;
+  base_eval<B, L>(p, s << L, L, r.V, r.H, r.F);
+  return r;
+}
+
 template <int B1, int B2, int CB1, int CB2, int L, int TPB>
 __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
@@ -180,7 +197,18 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
     const unsigned long long s = chunk_prefix(p, c);
     long long V;
     float H[B], F[NF];
+#if QB_CHUNK_START_NOINLINE
+    {
+      ChunkStart<B, NF> cs0 = chunk_start_ool<B, L>(p, s);
+      V = cs0.V;
+#pragma unroll
+      for (int i = 0; i < B; ++i) H[i] = cs0.H[i];
+#pragma unroll
+      for (int m = 0; m < NF; ++m) F[m] = cs0.F[m];
+    }
+#else
     base_eval<B, L>(p, s << L, L, V, H, F);
+#endif
     int dir;
     const unsigned long long key_hi = chunk_key(p, s, dir);
     long long cmin = LLONG_MAX, skip_min = LLONG_MAX;  // skip_min: least coarse value of a pruned block
