@@ -261,6 +261,7 @@ def run_reference(args, world, rank):
 def main():
     args = parse()
     world, rank, local = dist_setup(args.gpus)
+    os.environ["QB_DEVICE"] = str(local)  # the library's default device follows the rank -> GPU map
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
