@@ -195,7 +195,9 @@ static double sym(const double* c, int n, int i, int j) {
 
 // Integer scaling: q = rint(c * 2^e) with every partial sum the device forms below 2^24.
 // BE: block bits (their relative values are formed in fp32); B: table bits (T is built over them).
-static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false) {
+static long long seed_greedy(const std::vector<double>& q, int n);
+
+static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false, bool seed = false) {
   const double LIM = 16777215.0;  // 2^24 - 1
   auto bound = [&](auto get) {
     double r_in = 0.0, rmax = 0.0;
@@ -285,6 +287,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
 #endif
   while (std::ldexp(rq_in, -cs) + B + 2 > field_max) ++cs;
   P.coarse_shift = cs;
+  P.seed_val = seed ? seed_greedy(q, n) : LLONG_MAX;  // whole-space coarse searches only
   P.coarse_scale = (float)std::ldexp(1.0, -cs);
   const int bias = (int)field_max + 1;
   const double cscale = std::ldexp(1.0, -cs);  // exact power of two: x * cscale == ldexp(x, -cs)
@@ -314,6 +317,50 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
   P.tc_scale = (float)tscale;
   P.tc_bias = (int)std::ceil(r_h * tscale + 0.5 * B) - tcmin;
   return QB_OK;
+}
+
+// Greedy 1-flip descent on the quantized instance from a few starts: an attained value to start the
+// coarse kernel's pruning from (exact int64 arithmetic, O(n) per flip).  Only valid when the search
+// covers the whole space (the seed state must lie in it).
+static long long seed_greedy(const std::vector<double>& q, int n) {
+  long long seed = LLONG_MAX;
+  std::vector<long long> qi((size_t)n * n);
+  for (size_t t = 0; t < qi.size(); ++t) qi[t] = (long long)q[t];
+  auto sq = [&](int i, int j) { return i < j ? qi[(size_t)i * n + j] : qi[(size_t)j * n + i]; };
+  for (int start = 0; start < 3; ++start) {
+    unsigned long long x = start == 0 ? 0ull : (start == 1 ? ~0ull : 0x5555555555555555ull);
+    x &= mask64(n);
+    long long v = 0;
+    std::vector<long long> fld(n);  // fld[i] = q_ii + sum_{j != i} q_ij x_j (gain of setting bit i)
+    for (int i = 0; i < n; ++i) {
+      long long f = qi[(size_t)i * n + i];
+      for (int j = 0; j < n; ++j)
+        if (j != i && ((x >> j) & 1ull)) f += sq(i, j);
+      fld[i] = f;
+    }
+    for (int i = 0; i < n; ++i)
+      if ((x >> i) & 1ull) {
+        v += qi[(size_t)i * n + i];
+        for (int j = i + 1; j < n; ++j)
+          if ((x >> j) & 1ull) v += qi[(size_t)i * n + j];
+      }
+    for (int it = 0; it < 4 * n; ++it) {
+      int bi = -1;
+      long long bd = 0;
+      for (int i = 0; i < n; ++i) {
+        const long long d = ((x >> i) & 1ull) ? -fld[i] : fld[i];
+        if (d < bd) { bd = d; bi = i; }
+      }
+      if (bi < 0) break;
+      const long long sgn = ((x >> bi) & 1ull) ? -1 : 1;
+      x ^= 1ull << bi;
+      v += bd;
+      for (int j = 0; j < n; ++j)
+        if (j != bi) fld[j] += sgn * sq(j, bi);
+    }
+    seed = std::min(seed, v);
+  }
+  return seed;
 }
 
 static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& BE, int& L, bool tc = false) {
@@ -434,7 +481,10 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
                       (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC ||
                        (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   QB_TMARK("geometry");
-  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc)) return rc;
+  // the host seed must lie in the searched space: whole-space, unsharded coarse searches with short
+  // chunks (the kernel reads it only then)
+  const bool seed = coarse && m_fix == 0 && shard_count == 1 && n >= 24;
+  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed)) return rc;
   QB_TMARK("quantize");
 
   TableParams& P = *pl.P;

@@ -26,6 +26,9 @@ namespace qb {
 // (LDCU.128 = 8 states, broadcast through the operand path, not replicated per lane), and
 // VIMNMX3.U16x2 folds two candidate pairs into the running pair-minimum (4 states per min).
 constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw and Tc components
+#ifndef QB_SEED_MAX_LO
+#define QB_SEED_MAX_LO 30  // chunks of up to 2^LO blocks start from the host seed value (all; measured D -23%, E -0.2%)
+#endif
 #ifndef QB_LDC_MASK
 #define QB_LDC_MASK 0x4040  // table rows u (bit u) taking the per-lane LDC + VIADDMNMX path (measured)
 #endif
@@ -215,6 +218,10 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
     // pruning threshold: the better of this thread's best and the device-wide best so far (any
     // block whose bound exceeds a value some state attains holds neither a minimiser nor a tie)
     long long thr = min(best.val, gbest_dec(__ldcg(p.gbest)));
+    // short chunks: start from an attained value found on the host (greedy descent), so the first
+    // blocks of every thread are already filtered (pruning stays exact: that state's own block is
+    // never skipped, so it and its ties are still found)
+    if constexpr (LO <= QB_SEED_MAX_LO) thr = min(thr, p.seed_val);
     long long lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;  // prune when the coarse value exceeds it
     for (unsigned int j = 0; j < (1u << LO); ++j) {
       if (j) {

@@ -70,6 +70,7 @@ struct alignas(16) TableParams {
   unsigned Tc2[1 << (BMAX - 1)];  // coarse table pairs: Tc2[z/2] = (Tc(z) + 2^14) | (Tc(z+1) + 2^14) << 16
   float coarse_scale;        // 2^-s: coarse units per quantized unit
   int coarse_shift;          // s (coarse unit = 2^s quantized units); 0 = coarse is exact
+  long long seed_val;        // quantized value of a state found by host greedy descent (LLONG_MAX: none)
   float tc_scale;            // tensor-core pass (qb_tc.cuh): 2^-s_tc
   int tc_shift;              // s_tc: f16 coarse unit = 2^s_tc quantized units; 0 = exact
   int tc_bias;               // beta: added to every coarse table entry so all f16 results are >= 0
