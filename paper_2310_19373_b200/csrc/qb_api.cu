@@ -327,8 +327,19 @@ static long long seed_greedy(const std::vector<double>& q, int n) {
   std::vector<long long> qi((size_t)n * n);
   for (size_t t = 0; t < qi.size(); ++t) qi[t] = (long long)q[t];
   auto sq = [&](int i, int j) { return i < j ? qi[(size_t)i * n + j] : qi[(size_t)j * n + i]; };
-  for (int start = 0; start < 3; ++start) {
+#ifndef QB_SEED_STARTS
+#define QB_SEED_STARTS 3
+#endif
+  unsigned long long rs = 0x9E3779B97F4A7C15ull;  // splitmix64 stream for the extra starts
+  for (int start = 0; start < QB_SEED_STARTS; ++start) {
     unsigned long long x = start == 0 ? 0ull : (start == 1 ? ~0ull : 0x5555555555555555ull);
+    if (start >= 3) {
+      rs += 0x9E3779B97F4A7C15ull;
+      unsigned long long z = rs;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      x = z ^ (z >> 31);
+    }
     x &= mask64(n);
     long long v = 0;
     std::vector<long long> fld(n);  // fld[i] = q_ii + sum_{j != i} q_ij x_j (gain of setting bit i)
