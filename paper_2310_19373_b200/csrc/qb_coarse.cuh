@@ -14,6 +14,9 @@
 // blocks of a thread).  When s = 0 the coarse image is exact and no re-evaluation is needed.
 // The per-chunk minima written for the certified collect pass are lower bounds (exact for
 // evaluated blocks, the coarse bound for skipped ones), which keeps that pass complete.
+// Two of the 16 table rows (QB_LDC_MASK) load their table words per lane and fold with the fused
+// VIADDMNMX.U16x2, which trades issue slots for ALU-pipe work, and the
+// pruning threshold starts from a host-found attained value (p.seed_val, whole-space searches).
 #pragma once
 #include "qb_table.cuh"
 
