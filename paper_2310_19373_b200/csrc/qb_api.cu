@@ -494,7 +494,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   QB_TMARK("geometry");
   // the host seed must lie in the searched space: whole-space, unsharded coarse searches with short
   // chunks (the kernel reads it only then)
-  const bool seed = coarse && m_fix == 0 && shard_count == 1 && n >= 24;
+  const bool seed = (coarse || tc) && m_fix == 0 && shard_count == 1 && n >= 24;
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed)) return rc;
   QB_TMARK("quantize");
 

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(TC_TPB, TC_CTAS_PER_SM) tc_kernel(const __grid
         base_eval<B, L>(p, s << L, L, V, H, F);
         key_hi = chunk_key(p, s, dir);
         // a new chunk starts from the device-wide best (the thread's own best is in it too)
-        thr = min(best.val, gbest_dec(__ldcg(p.gbest)));
+        thr = min(min(best.val, gbest_dec(__ldcg(p.gbest))), p.seed_val);  // host seed: whole-space searches
         lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;
       } else {
 #pragma unroll
