@@ -36,7 +36,7 @@ constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw 
 #define QB_LDC_MASK 0x4040  // table rows u (bit u) taking the per-lane LDC + VIADDMNMX path (measured)
 #endif
 #ifndef QB_EXACT_NOINLINE
-#define QB_EXACT_NOINLINE 1  // long chunks call the exact re-evaluation out of line (measured n=40: 52 -> 41 ms)
+#define QB_EXACT_NOINLINE 0  // 1: long chunks call the exact re-evaluation out of line (won 52 -> 41 ms before the host seed; inline measured 33.99 -> 33.70 ms since)
 #endif
 
 // exact fp32 re-evaluation of one block, out of line (rare path: keeps its 64 live table-loop
