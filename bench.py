@@ -47,7 +47,7 @@ ALU_PEAKS = os.path.join(ROOT, "profiles", "r01_alu_peaks.json")
 FP32_ADD_LANES_PER_SM_CLK = 128.0
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
 # ncu --set full capture of the search kernel (DRAM bytes per launch, n=40 config E)
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r10_ncu_search_summary.txt")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r11_ncu_search_summary.txt")
 
 
 def ncu_traffic_bytes():
@@ -67,7 +67,7 @@ def ncu_traffic_bytes():
 
 
 # SASS instructions per state of the table kernel's inner block (cuobjdump count)
-SASS_INSTR_PER_STATE = 1.033  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r10_ncu_search_summary.txt)
+SASS_INSTR_PER_STATE = 1.032  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r11_ncu_search_summary.txt)
 
 
 def parse():
