@@ -374,7 +374,8 @@ static long long seed_greedy(const std::vector<double>& q, int n) {
   return seed;
 }
 
-static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int& BE, int& L, bool tc = false) {
+static int choose_geometry(int n, int m_fix, int m_lock, uint32_t shard_count, int sms, int& BE, int& L,
+                           bool tc = false) {
   const int lmax = n - m_lock;  // free bits available per chunk
   if (lmax < 1) return fail(QB_E_ARG, "no free bits");
   if (lmax <= BIG_BE) {
@@ -392,7 +393,9 @@ static int choose_geometry(int n, int m_lock, uint32_t shard_count, int sms, int
 #endif
   const double want_chunks = tc ? (double)QB_TC_ROUNDS * sms * TC_CTAS_PER_SM * TC_WORKERS * (double)shard_count
                                 : (double)QB_CHUNKS_PER_THREAD * sms * QB_MINB * TPB * (double)shard_count;
-  int want_k = m_lock + (int)std::ceil(std::log2(std::max(1.0, want_chunks)));
+  // the chunk count tracks the states actually searched (2^(n - m_fix)); the tie rule only needs the
+  // chunk prefix to cover the m_tie suffix bits (k >= m_tie), not m_tie extra bits on top
+  int want_k = std::max(m_lock, m_fix + (int)std::ceil(std::log2(std::max(1.0, want_chunks))));
   int Lw = n - want_k;
   if (Lw & 1) Lw += (Lw < 16) ? 1 : -1;  // even chunk sizes: round up for small, down for large chunks
   Lw = std::max(Lw, tc ? std::min(14, lmax) : BIG_BE);  // tensor-core kernels exist for L >= 14
@@ -425,7 +428,8 @@ static unsigned long long ordered_double(double v) {
 }
 
 static double eval_upper(const double* c, int n, const double* x) {
-  // _kernels.py:12-20, same order; this TU is compiled with --fmad=false for the host too.
+  // _kernels.py:12-20, same order.  Host code of this TU is built with -Xcompiler -ffp-contract=off
+  // (_lib.NVCC_FLAGS), which keeps the multiply and add unfused and hence bit-identical to the reference.
   double acc = 0.0;
   for (int i = 0; i < n; ++i)
     for (int j = i; j < n; ++j) acc += c[(size_t)i * n + j] * x[i] * x[j];
@@ -474,7 +478,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const int m_lock = std::max(m_fix, m_tie);
   int BE, L;
   const bool want_tc = variant == QB_VARIANT_TC;
-  if (int rc = choose_geometry(n, m_lock, shard_count, dev->sms, BE, L, want_tc)) return rc;
+  if (int rc = choose_geometry(n, m_fix, m_lock, shard_count, dev->sms, BE, L, want_tc)) return rc;
   pl.BE = BE;
   pl.L = L;
   pl.k = n - L;
@@ -492,9 +496,10 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
                       (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC ||
                        (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   QB_TMARK("geometry");
-  // the host seed must lie in the searched space: whole-space, unsharded coarse searches with short
-  // chunks (the kernel reads it only then)
-  const bool seed = (coarse || tc) && m_fix == 0 && shard_count == 1 && n >= 24;
+  // the host seed must be a value some searched state attains: whole-space searches (m_fix == 0) of the
+  // coarse and tensor-core kernels, any chunk length; shards use it too (the combine treats a shard
+  // that finds nothing <= the seed as empty, see the shard handling below)
+  const bool seed = (coarse || tc) && m_fix == 0 && n >= 24;
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed)) return rc;
   QB_TMARK("quantize");
 
@@ -558,7 +563,11 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const bool collect = !pl.exact || all_out != nullptr;
   P.mode = collect ? MODE_SEARCH_RECORD : MODE_SEARCH;
   if (collect) {
-    if (nchunks > (1ull << 27)) return fail(QB_E_INTERNAL, "too many chunks for the approximate path");
+    // one 8-byte chunk minimum per chunk: up to 8 GB of HBM (k - m_fix <= 30, i.e. tie suffixes of up to
+    // 30 bits at n = 40 -- the chunk prefix must cover the m_tie suffix bits)
+    if (nchunks > (1ull << 30))
+      return fail(QB_E_INTERNAL, "certified path limited to 2^30 chunks (fixed_bits too large for n=" +
+                                     std::to_string(n) + ")");
     if (int rc = ensure(&dev->d_chunk_min, &dev->chunk_min_cap, (size_t)nchunks)) return rc;
     P.chunk_min = dev->d_chunk_min;
     if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)1 << 20)) return rc;
@@ -627,7 +636,15 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->search_ms = ms;
   out->collect_ms = collect ? out->kernel_ms - out->search_ms : 0.0;
   const FinalOut fo = *dev->h_final;
-  if (!fo.found) return fail(QB_E_INTERNAL, "search found no state attaining the block minimum");
+  if (!fo.found) {
+    if (seed && shard_count > 1 && fo.val == LLONG_MAX) {
+      // every block of this shard was certified above the seed value, which some state of another shard
+      // attains: the shard holds neither the minimum nor a tie -> empty result (keys ~0, the combine skips it)
+      out->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+      return QB_OK;
+    }
+    return fail(QB_E_INTERNAL, "search found no state attaining the block minimum");
+  }
 
   if (!collect) {
     out->argmin_bits = fo.x;
@@ -637,13 +654,29 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     if (host_tie_key(fo.x, n, m_tie, rule) != fo.key)
       return fail(QB_E_INTERNAL, "device tie key disagrees with the host tie key");
   } else {
-    if (dev->h_counts[0] > P.list_cap || dev->h_counts[1] > P.list_cap)
-      return fail(QB_E_INTERNAL, "collect pass: more than " + std::to_string(P.list_cap) +
-                                     " chunks or blocks within the certified bound");
+    bool recollected = false;
+    if (dev->h_counts[0] > P.list_cap || dev->h_counts[1] > P.list_cap) {
+      // more chunks / blocks within the certified bound than the lists hold (e.g. a huge diagonal term
+      // with many weights that quantize to 0): grow the lists to the counted sizes and collect again
+      const unsigned long long need = std::max(dev->h_counts[0], dev->h_counts[1]);
+      if (need > (1ull << 31))
+        return fail(QB_E_INTERNAL, "collect pass: " + std::to_string(need) + " blocks within the certified bound");
+      if (int rc = ensure(&dev->d_lists, &dev->list_cap, (size_t)(2 * need))) return rc;
+      P.list_cap = dev->list_cap / 2;
+      P.chunk_list = dev->d_lists;
+      P.block_list = dev->d_lists + P.list_cap;
+      QB_CUDA(cudaMemsetAsync(dev->d_counts, 0, 3 * sizeof(unsigned long long), st));
+      if (int rc = enqueue_collect()) return rc;
+      QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              st));
+      QB_CUDA(cudaStreamSynchronize(st));
+      if (dev->h_counts[0] > P.list_cap || dev->h_counts[1] > P.list_cap)
+        return fail(QB_E_INTERNAL, "collect pass: list counts changed between identical passes");
+      recollected = true;
+    }
     unsigned long long cnt = dev->h_counts[2];
     if (cnt == 0) return fail(QB_E_INTERNAL, "collect pass found no candidate");
     const size_t prefetched = std::min<size_t>(kCandPre, dev->cand_cap);  // read back with the counts
-    bool recollected = false;
     if (cnt > P.cand_cap && all_out != nullptr && cnt <= (1ull << 27)) {
       // all-minimisers request with more ties than the buffer holds: grow it and collect again
       if (int rc = ensure(&dev->d_cand, &dev->cand_cap, (size_t)cnt)) return rc;
@@ -932,7 +965,7 @@ int qb_solve_devices(const double* coeffs, int n, int m_fix, uint64_t suffix, in
         (parts[i].value_key == parts[w].value_key && parts[i].tie_key < parts[w].tie_key))
       w = i;
   }
-  if (w < 0) return qb::fail(QB_E_INTERNAL, "no shard scanned any state");
+  if (w < 0 || parts[w].value_key == ~0ull) return qb::fail(QB_E_INTERNAL, "no shard produced a result");
   qb_result r = parts[w];
   r.states = 0;
   r.candidates = 0;

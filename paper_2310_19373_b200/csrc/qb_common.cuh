@@ -111,7 +111,8 @@ __device__ __forceinline__ long long gbest_dec(unsigned long long e) {
 // Collect threshold: the search's quantized minimum (written by its last CTA) plus the certified
 // margin; read from the device so the collect pass is enqueued without a host round trip.
 __device__ __forceinline__ long long collect_theta(const TableParams& p) {
-  return __ldcg(&p.final_out->val) + p.theta_add;
+  const long long v = __ldcg(&p.final_out->val);
+  return v == LLONG_MAX ? LLONG_MIN : v + p.theta_add;  // LLONG_MAX: the search found nothing (empty shard)
 }
 enum { MODE_SEARCH = 0, MODE_SEARCH_RECORD = 1, MODE_COLLECT = 2, MODE_REDUCE_VALUE = 3, MODE_REDUCE_KEY = 4 };
 

@@ -93,6 +93,14 @@ class SolveConfig:
             object.__setattr__(self, "devices", tuple(int(d) for d in devs))
 
 
+def _devices_of(config):
+    """The ``devices`` knob of a config, or None.  The reference's own ``SolveConfig``
+    (solver.py:82-96) has no such field: any object with ``threads`` / ``fixed_bits`` / ``mode``
+    is accepted (duck typing, so the reference's types pass through Seam 2 unchanged)."""
+    devs = getattr(config, "devices", None) if config is not None else None
+    return None if devs is None else SolveConfig(devices=devs).devices
+
+
 def _gpu_solve(coeffs, m_fix: int, suffix: int, m_tie: int, rule: int, devices=None):
     """One solve on the current device, or sharded over ``devices`` (one shard per entry)."""
     if devices is None:
@@ -181,7 +189,7 @@ def solve_parallel(instance: QuboInstance, config: SolveConfig | None = None) ->
     """All 2^m subspaces in one GPU launch, lowest-suffix tie rule (solver.py:193-229)."""
     m = _resolve_m(instance, config)
     t0 = time.perf_counter()
-    res = _gpu_solve(instance.coeffs, 0, 0, m, _lib.TIE_GRAY, config.devices if config is not None else None)
+    res = _gpu_solve(instance.coeffs, 0, 0, m, _lib.TIE_GRAY, _devices_of(config))
     return _solution(instance, res, (1 << instance.n) - (1 << m), t0)
 
 
@@ -255,5 +263,5 @@ def solve(instance: QuboInstance, config: SolveConfig | None = None) -> Solution
     if config.mode == "naive":
         return solve_naive(instance)
     if config.mode == "incremental":
-        return solve_incremental(instance, devices=config.devices)
+        return solve_incremental(instance, devices=_devices_of(config))
     return solve_parallel(instance, config)

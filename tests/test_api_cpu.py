@@ -83,3 +83,48 @@ def test_solve_config_devices_validation():
     for bad in ([], [-1], ["0"]):
         with pytest.raises(ValueError):
             qb.SolveConfig(devices=bad)
+
+
+def test_step_level_drift_pinned_to_reference(golden):
+    """Acceptance criterion 2 shape (reference test_acceptance.py:56-73): the running value after each
+    Eq. 3 ``delta`` along the Gray walk, bit-identical to the reference's own trace (every 97th step
+    of the n=12 walk, tests/golden/reference_golden.json ``delta_trace_n12``), and within 1e-9 of the
+    direct evaluation at every step."""
+    tr = golden["delta_trace_n12"]
+    inst = qb.QuboInstance(np.array(tr["coeffs"]))
+    form = qb.split(inst)
+    want = {k: (l, v, d) for k, l, v, d in tr["samples"]}
+    x = np.zeros(12, dtype=np.uint8)
+    v = 0.0
+    seen = 0
+    for k, l in enumerate(qb.flip_sequence(12), start=1):
+        x[l] ^= 1
+        v += qb.delta(form, x, l)
+        if k in want:
+            wl, wv, wd = want[k]
+            assert (l, v) == (wl, wv), k
+            assert qb.evaluate(inst, x) == wd
+            seen += 1
+        assert abs(v - qb.evaluate(inst, x)) <= 1e-9
+    assert seen == len(want) > 40
+
+
+def test_step_level_drift_full_traces():
+    """The same pin at every one of the 4095 steps, for two instances (make_golden_extra.py)."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "reference_golden_extra.json")
+    with open(path) as fh:
+        traces = json.load(fh)["drift_traces"]
+    for tr in traces:
+        inst = qb.random_instance(tr["n"], tr["seed"])
+        form = qb.split(inst)
+        x = np.zeros(tr["n"], dtype=np.uint8)
+        v = 0.0
+        for k, l in enumerate(qb.flip_sequence(tr["n"])):
+            x[l] ^= 1
+            v += qb.delta(form, x, l)
+            assert l == tr["flips"][k]
+            assert v == float.fromhex(tr["running_hex"][k]), k
+            assert qb.evaluate(inst, x) == float.fromhex(tr["direct_hex"][k]), k
