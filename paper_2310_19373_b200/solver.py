@@ -27,7 +27,7 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from .core import MAX_DIM, DimensionCapError, QuboInstance, bits_from_int
+from .core import MAX_DIM, DimensionCapError, QuboInstance, bits_from_int, cap_error
 
 # solver.py:33
 NAIVE_MAX_DIM = 24
@@ -120,12 +120,13 @@ def _solution(inst: QuboInstance, res, evaluations: int, t0: float) -> Solution:
 def solve_naive(instance: QuboInstance, *, max_n: int = NAIVE_MAX_DIM) -> Solution:
     """Exhaustive search keeping the lowest-integer minimiser (solver.py:99-115)."""
     if instance.n > max_n:
-        raise DimensionCapError(
+        raise cap_error(
+            instance,
             f"n={instance.n} exceeds the naive-solver guard {max_n}; "
-            f"use the incremental solver, or raise max_n to force it"
+            f"use the incremental solver, or raise max_n to force it",
         )
     if instance.n > MAX_DIM:
-        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+        raise cap_error(instance, f"n={instance.n} exceeds cap {MAX_DIM}")
     t0 = time.perf_counter()
     res = _lib.solve(instance.coeffs, 0, 0, 0, _lib.TIE_INTEGER)
     return _solution(instance, res, (1 << instance.n) - 1, t0)
@@ -135,7 +136,7 @@ def solve_incremental(instance: QuboInstance, *, devices=None) -> Solution:
     """Exhaustive Gray-code solve; ties to the lowest global Gray rank (solver.py:118-136).
     ``devices``: optional CUDA devices to shard over (extension; see SolveConfig)."""
     if instance.n > MAX_DIM:
-        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+        raise cap_error(instance, f"n={instance.n} exceeds cap {MAX_DIM}")
     if devices is not None:
         devices = SolveConfig(devices=devices).devices
     t0 = time.perf_counter()
@@ -149,7 +150,7 @@ def solve_subspace(instance: QuboInstance, sub: SubspaceSpec) -> Solution:
     if sub.m >= instance.n:
         raise ValueError(f"cannot fix {sub.m} bits of an n={instance.n} instance")
     if instance.n > MAX_DIM:
-        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+        raise cap_error(instance, f"n={instance.n} exceeds cap {MAX_DIM}")
     res = _lib.solve(instance.coeffs, sub.m, sub.suffix, sub.m, _lib.TIE_GRAY)
     return _solution(instance, res, (1 << (instance.n - sub.m)) - 1, t0)
 
@@ -176,7 +177,7 @@ def _resolve_m(instance: QuboInstance, config: SolveConfig | None) -> int:
     if instance.n < 2:
         raise ValueError("parallel solving needs n >= 2")
     if instance.n > MAX_DIM:
-        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+        raise cap_error(instance, f"n={instance.n} exceeds cap {MAX_DIM}")
     m = config.fixed_bits
     if m is None:
         m = default_fixed_bits(instance.n, config.threads)
@@ -247,7 +248,7 @@ def all_minimizers(instance: QuboInstance, config: SolveConfig | None = None, *,
     The reference returns a single minimiser (SPEC.md:273 non-goal); this is an extension.
     Raises if more than ``max_count`` minimisers exist."""
     if instance.n > MAX_DIM:
-        raise DimensionCapError(f"n={instance.n} exceeds cap {MAX_DIM}")
+        raise cap_error(instance, f"n={instance.n} exceeds cap {MAX_DIM}")
     m = _resolve_m(instance, config) if (config is not None and config.mode == "parallel") else 0
     value, xs, count = _lib.all_minimisers(instance.coeffs, 0, 0, m, cap=max_count)
     if count > max_count:

@@ -60,6 +60,13 @@ try:
     b2.solve_parallel(inst, qubrute.SolveConfig(threads=1, fixed_bits=8))
 except ValueError as e:
     print("valueerror", e)
+big = qubrute.QuboInstance(np.zeros((41, 41)), max_n=41)
+for call in (lambda: b2.solve_incremental(big), lambda: b2.solve_naive(qubrute.random_instance(10, seed=1), max_n=8)):
+    try:
+        call()
+    except qubrute.DimensionCapError as e:
+        assert isinstance(e, b2.DimensionCapError)
+        print("caperror")
 """
     r = subprocess.run([sys.executable, "-c", code], env=_ref_env(), capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
@@ -67,6 +74,7 @@ except ValueError as e:
     assert "AttributeError" not in r.stderr
     assert lines.count("ran") + lines.count("backend") == 3, r.stdout
     assert "valueerror" in r.stdout
+    assert lines.count("caperror") == 2, r.stdout  # reference-typed cap errors (test_solver.py:55-58,102-105)
 
 
 def _run_suite(seam: str, tmp_path):

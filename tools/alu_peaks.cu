@@ -7,12 +7,14 @@
 //
 // Each kernel keeps 16 independent dependency chains per thread, 2 CTAs x 512 threads per SM
 // (32 warps/SM), ~2-5 ms per launch.  Reported per kernel: lane-ops/s from CUDA events over the
-// launch, the SM clock from %clock64 / event time, and lane-ops per SM per clock.
+// launch (many back-to-back launches); tools/alu_peaks.py runs one kernel per process while
+// nvidia-smi samples the SM clock and converts to per-SM-per-clock figures with the sampled clock.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/alu_peaks tools/alu_peaks.cu
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #define CK(x)                                                                                 \
   do {                                                                                        \
@@ -33,15 +35,15 @@ __device__ __forceinline__ long long clk() {
   return c;
 }
 
-enum { K_FADD, K_FADD2, K_FFMA, K_FMNMX3, K_DADD, K_IADD3, K_VIMNMX3, K_MIX, K_VIADD16, K_VMIN3_16, K_MIX16, K_NK };
+enum { K_FADD, K_FADD2, K_FFMA, K_FMNMX3, K_DADD, K_IADD3, K_VIMNMX3, K_MIX, K_VIADD16, K_VMIN3_16, K_MIX16, K_ISSUE, K_NK };
 static const char* NAMES[K_NK] = {"fadd", "fadd2", "ffma", "fmnmx3", "dadd", "iadd3", "vimnmx3",
                                   "mix_fadd2_fmnmx3_ldcu128", "viadd_16x2", "vimnmx3_s16x2",
-                                  "mix16_viadd2_vimnmx3_ldcu128"};
+                                  "mix16_viadd2_vimnmx3_ldcu128", "issue_ffma_iadd3"};
 // lane-operations per instruction: FADD2 / IADD3 = 2 adds, FMNMX3 / VIMNMX3 = 2 two-input mins,
 // MIX counts states (one FADD2 + one FMNMX3 per 2 states)
-static const double OPS[K_NK] = {1, 2, 1, 2, 1, 2, 2, 2, 2, 4, 2};
+static const double OPS[K_NK] = {1, 2, 1, 2, 1, 2, 2, 2, 2, 4, 2, 1};
 // MIX16 per iteration: 8 VIADD.16x2 (16 states) + 4 VIMNMX3.S16x2; counted as 8 "instructions" of 2 states
-static const int INSTR_PER_ITER[K_NK] = {CH, CH / 2, CH, CH, CH, CH, CH, CH / 2, CH, CH, CH / 2};
+static const int INSTR_PER_ITER[K_NK] = {CH, CH / 2, CH, CH, CH, CH, CH, CH / 2, CH, CH, CH / 2, 2 * CH};
 
 struct Tab {
   float t[2048];
@@ -90,6 +92,25 @@ __global__ void __launch_bounds__(TPB, 2) kern(const __grid_constant__ Tab tab, 
     }
 #pragma unroll
     for (int i = 0; i < CH; i++) acc += (float)(v[i] & 0xffff);
+  } else if constexpr (K == K_ISSUE) {
+    // issue-slot peak: every iteration issues one FFMA (FMA pipe) and one IADD3 (ALU pipe) per chain,
+    // independent pipes at rt_SMSP = 2 each, so the SMSP can issue one instruction per clock
+    float f[CH];
+    int v[CH];
+#pragma unroll
+    for (int i = 0; i < CH; i++) {
+      f[i] = threadIdx.x * 0.5f + i;
+      v[i] = threadIdx.x * (i + 3);
+    }
+    for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+      for (int i = 0; i < CH; i++) {
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(f[(i + 1) % CH]), "f"(f[(i + 3) % CH]));
+        asm volatile("{ .reg .s32 t; add.s32 t, %0, %1; add.s32 %0, t, %2; }" : "+r"(v[i]) : "r"(v[(i + 1) % CH]), "r"(v[(i + 2) % CH]));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CH; i++) acc += f[i] + (float)v[i];
   } else if constexpr (K == K_IADD3 || K == K_VIMNMX3) {
     int v[CH];
 #pragma unroll
@@ -149,43 +170,38 @@ __global__ void __launch_bounds__(TPB, 2) kern(const __grid_constant__ Tab tab, 
 }
 
 template <int K>
-int run(int sms, float* dout, long long* dcyc, const Tab& tab, bool first) {
+int run(int sms, float* dout, long long* dcyc, const Tab& tab, int launches) {
   const int grid = sms * 2;
   kern<K><<<grid, TPB>>>(tab, dout, dcyc);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  float best_ms = 1e30f;
-  for (int rep = 0; rep < 3; rep++) {
-    cudaEventRecord(e0);
-    kern<K><<<grid, TPB>>>(tab, dout, dcyc);
-    cudaEventRecord(e1);
-    CK(cudaEventSynchronize(e1));
-    float ms;
-    cudaEventElapsedTime(&ms, e0, e1);
-    if (ms < best_ms) best_ms = ms;
-  }
-  long long* h = new long long[grid];
-  CK(cudaMemcpy(h, dcyc, sizeof(long long) * grid, cudaMemcpyDeviceToHost));
-  double mean = 0;
-  for (int i = 0; i < grid; i++) mean += (double)h[i];
-  mean /= grid;
-  delete[] h;
-  const double instr = (double)ITERS * INSTR_PER_ITER[K] * TPB * grid;  // thread-instructions
-  const double lane_ops = instr * OPS[K];
-  const double ops_s = lane_ops / (best_ms * 1e-3);
-  const double mhz = mean / (best_ms * 1e3);  // in-kernel cycles per microsecond of launch
-  const double per_sm_clk = lane_ops / grid * 2 / mean;
-  const double warp_instr_sm_clk = instr / 32.0 / grid * 2 / mean;
-  printf("%s\"%s\": {\"lane_ops_per_s\": %.4e, \"lane_ops_per_sm_clk\": %.1f, \"warp_instr_per_sm_clk\": %.3f, "
-         "\"ms\": %.3f, \"implied_sm_mhz\": %.0f}",
-         first ? "" : ", ", NAMES[K], ops_s, per_sm_clk, warp_instr_sm_clk, best_ms, mhz);
+  // back to back for `launches` launches (long enough for nvidia-smi to sample the SM clock)
+  cudaEventRecord(e0);
+  for (int rep = 0; rep < launches; rep++) kern<K><<<grid, TPB>>>(tab, dout, dcyc);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double per_launch_ms = ms / launches;
+  const double instr = (double)ITERS * INSTR_PER_ITER[K] * TPB * grid;  // thread-instructions per launch
+  printf("{\"kernel\": \"%s\", \"launches\": %d, \"ms_per_launch\": %.5f, \"thread_instr_per_launch\": %.6e, "
+         "\"lane_ops_per_instr\": %.1f, \"lane_ops_per_s\": %.5e, \"warp_instr_per_s\": %.5e, \"sms\": %d}\n",
+         NAMES[K], launches, per_launch_ms, instr, OPS[K], instr * OPS[K] / (per_launch_ms * 1e-3),
+         instr / 32.0 / (per_launch_ms * 1e-3), sms);
   fflush(stdout);
   return 0;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    printf("usage: alu_peaks <kernel index 0..%d> [launches]\n", K_NK - 1);
+    for (int k = 0; k < K_NK; k++) printf("  %d %s\n", k, NAMES[k]);
+    return 2;
+  }
+  const int k = atoi(argv[1]);
+  const int launches = argc > 2 ? atoi(argv[2]) : 400;
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
   const int sms = prop.multiProcessorCount;
@@ -195,21 +211,19 @@ int main() {
   CK(cudaMalloc(&dcyc, sizeof(long long) * sms * 2));
   static Tab tab;
   for (int i = 0; i < 2048; i++) tab.t[i] = (float)(i % 97) - 40.f;
-  printf("{\"gpu\": \"%s\", \"sms\": %d, \"threads_per_sm\": %d, \"chains_per_thread\": %d, "
-         "\"method\": \"2 CTAs x 512 threads per SM, 16 independent chains/thread, %d iterations, best of 3 "
-         "launches (CUDA events); per-SM-clock figures from %%clock64 inside the kernel\", \"results\": {",
-         prop.name, sms, 2 * TPB, CH, ITERS);
-  run<K_FADD>(sms, dout, dcyc, tab, true);
-  run<K_FADD2>(sms, dout, dcyc, tab, false);
-  run<K_FFMA>(sms, dout, dcyc, tab, false);
-  run<K_FMNMX3>(sms, dout, dcyc, tab, false);
-  run<K_DADD>(sms, dout, dcyc, tab, false);
-  run<K_IADD3>(sms, dout, dcyc, tab, false);
-  run<K_VIMNMX3>(sms, dout, dcyc, tab, false);
-  run<K_MIX>(sms, dout, dcyc, tab, false);
-  run<K_VIADD16>(sms, dout, dcyc, tab, false);
-  run<K_VMIN3_16>(sms, dout, dcyc, tab, false);
-  run<K_MIX16>(sms, dout, dcyc, tab, false);
-  printf("}}\n");
-  return 0;
+  switch (k) {
+    case K_FADD: return run<K_FADD>(sms, dout, dcyc, tab, launches);
+    case K_FADD2: return run<K_FADD2>(sms, dout, dcyc, tab, launches);
+    case K_FFMA: return run<K_FFMA>(sms, dout, dcyc, tab, launches);
+    case K_FMNMX3: return run<K_FMNMX3>(sms, dout, dcyc, tab, launches);
+    case K_DADD: return run<K_DADD>(sms, dout, dcyc, tab, launches);
+    case K_IADD3: return run<K_IADD3>(sms, dout, dcyc, tab, launches);
+    case K_VIMNMX3: return run<K_VIMNMX3>(sms, dout, dcyc, tab, launches);
+    case K_MIX: return run<K_MIX>(sms, dout, dcyc, tab, launches);
+    case K_VIADD16: return run<K_VIADD16>(sms, dout, dcyc, tab, launches);
+    case K_VMIN3_16: return run<K_VMIN3_16>(sms, dout, dcyc, tab, launches);
+    case K_MIX16: return run<K_MIX16>(sms, dout, dcyc, tab, launches);
+    case K_ISSUE: return run<K_ISSUE>(sms, dout, dcyc, tab, launches);
+  }
+  return 2;
 }
