@@ -41,33 +41,120 @@ CONFIG_DESC = {
     "D": "D: n=32 int32 U[-1000,1000], single instance",
     "E": "E: n=40 fp32 N(0,1), 10% off-diagonal density, dense diagonal",
 }
-# FP32 add-lane peak: measured on this pool's B200 by tools/alu_peaks.cu (profiles/r01_alu_peaks.json,
-# CUDA events, 2 CTAs x 512 threads/SM); fallback = 128 lanes/SM/clk x SMs x max SM clock
-ALU_PEAKS = os.path.join(ROOT, "profiles", "r01_alu_peaks.json")
-FP32_ADD_LANES_PER_SM_CLK = 128.0
+# Roofline inputs.  The path is ALU-issue bound (0 algorithmic HBM bytes per state):
+# * the issue-slot peak in warp-instructions per SM per clock is MEASURED by tools/alu_peaks.py
+#   (FFMA + IADD3 on independent pipes, nvidia-smi-sampled clock); fallback 4 (one per SMSP per clock);
+# * the instructions the dominant kernel issues per state come from an ncu capture of that kernel
+#   (tools/ncu_summary.py --record), keyed by the sha256 of its SASS in the library that ran: if the
+#   kernel changed since the capture, the issue figures are withheld rather than reported stale.
+ALU_PEAKS = os.path.join(ROOT, "profiles", "r12_alu_peaks.json")
 ISSUE_WARP_INSTR_PER_SM_CLK = 4.0
-# ncu --set full capture of the search kernel (DRAM bytes per launch, n=40 config E)
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r11_ncu_search_summary.txt")
+FP32_ADD_LANES_PER_SM_CLK = 128.0
+KERNEL_RECORDS = os.path.join(ROOT, "profiles", "kernel_records.json")
 
 
-def ncu_traffic_bytes():
-    """dram__bytes_read.sum + dram__bytes_write.sum of the committed capture, in bytes, or None."""
-    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+def kernel_symbol(lib_path: str, family: str, L: int):
+    """Mangled name of ``qb::<family><..., L, ...>`` in the library (5th template argument = L)."""
+    import re
+
     try:
-        vals = {}
-        with open(NCU_SUMMARY) as fh:
-            for line in fh:
-                if line.startswith("dram__bytes_read.sum =") or line.startswith("dram__bytes_write.sum ="):
-                    k, rest = line.split("=")
-                    num, unit = rest.split()
-                    vals[k.strip()] = float(num) * scale[unit]
-        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
-    except (OSError, KeyError, ValueError):
+        out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True,
+                             timeout=60).stdout
+    except (OSError, subprocess.SubprocessError):
         return None
+    pat = re.compile(r"_ZN2qb%d%sI(?:Li\d+E){4}Li%dE(?:Li\d+E)*EEvNS_\w+E$" % (len(family), family, L))
+    for line in out.split("\n"):
+        parts = line.split()
+        if parts and pat.match(parts[-1]):
+            return parts[-1]
+    return None
 
 
-# SASS instructions per state of the table kernel's inner block (cuobjdump count, DESIGN.md §4)
-SASS_INSTR_PER_STATE = 1.032  # ncu smsp__inst_executed x 32 / 2^40 of the coarse kernel (profiles/r11_ncu_search_summary.txt)
+def sass_sha256(lib_path: str, symbol: str):
+    """sha256 of the SASS instruction text of one kernel in the library (cuobjdump), or None."""
+    import hashlib
+
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", "-fun", symbol, lib_path], capture_output=True, text=True,
+                             timeout=120).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    body = [ln.strip() for ln in out.split("\n") if ln.strip().startswith("/*") and "*/" in ln]
+    if not body:
+        return None
+    return hashlib.sha256("\n".join(body).encode()).hexdigest()
+
+
+def kernel_record(sha):
+    """The committed ncu record (instr/state, DRAM bytes, issue activity) for this SASS, or None."""
+    try:
+        with open(KERNEL_RECORDS) as fh:
+            recs = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    return recs.get(sha) if sha else None
+
+
+def issue_peak_per_sm_clk():
+    """(warp-instructions issued per SM per clock, source) -- measured, else the architectural 4."""
+    try:
+        with open(ALU_PEAKS) as fh:
+            rec = json.load(fh)["results"]["issue_ffma_iadd3"]
+        return float(rec["warp_instr_per_sm_clk"]), f"measured ({os.path.relpath(ALU_PEAKS, ROOT)}: FFMA+IADD3 " \
+            f"issue at {rec['sm_mhz_sampled']:.0f} MHz sampled)"
+    except (OSError, KeyError, ValueError, TypeError):
+        return ISSUE_WARP_INSTR_PER_SM_CLK, "fallback: 4 warp-instr/SM/clk (1 per SMSP per clock)"
+
+
+def fp32_lane_peak_per_sm_clk():
+    try:
+        with open(ALU_PEAKS) as fh:
+            rec = json.load(fh)["results"]["fadd2"]
+        return float(rec["lane_ops_per_sm_clk"]), "measured FADD2 lane rate"
+    except (OSError, KeyError, ValueError, TypeError):
+        return FP32_ADD_LANES_PER_SM_CLK, "fallback 128 FP32 lanes/SM/clk"
+
+
+FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel"}
+
+
+def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path):
+    """Issue-slot roofline of the search kernel (the path is ALU-issue bound).
+
+    achieved = per-launch states x (instructions per state, from the ncu record of THIS kernel's
+    SASS) / 32 / the launch's CUDA-event time; peak = measured issue rate per SM per clock x SMs x
+    the SM clock sampled during the timed region.  ``nominal_frac`` keeps SURVEY.md §8d's n+1
+    ops/state basis against the measured FP32 lane rate: > 1 because the table method forms a
+    state's value with ~1 instruction instead of n+1 additions."""
+    L = n - int(r.prefix_bits)
+    family = FAMILIES.get(int(r.variant))
+    sym = kernel_symbol(lib_path, family, L) if family else None
+    sha = sass_sha256(lib_path, sym) if sym else None
+    rec = kernel_record(sha)
+    ipc, ipc_src = issue_peak_per_sm_clk()
+    lanes, lanes_src = fp32_lane_peak_per_sm_clk()
+    issue_peak = ipc * sm_count * sm_hz  # warp-instructions / s
+    nominal_peak = lanes * sm_count * sm_hz
+    nominal_achieved = per_launch_states * (n + 1) / search_s
+    out = {"bound": "alu-issue", "unit": "Gwarp-instr/s", "achieved": None, "peak": issue_peak / 1e9, "frac": None,
+           "traffic": None, "kernel": sym, "sass_sha256": sha, "search_ms_per_launch": search_s * 1e3,
+           "peak_basis": f"{ipc:.3f} warp-instr/SM/clk {ipc_src} x {sm_count} SMs x {sm_hz / 1e6:.0f} MHz "
+                         "(SM clock sampled during the timed region)",
+           "nominal_frac": nominal_achieved / nominal_peak,
+           "nominal_basis": f"{n + 1} ops/state (SURVEY.md §8d: n-1 field adds + 1 value add + 1 min) vs "
+                            f"{lanes:.1f} FP32 lanes/SM/clk ({lanes_src}); > 1 = the table method's algorithmic saving"}
+    if rec is None:
+        out["note"] = ("no ncu record for this kernel's SASS in profiles/kernel_records.json (kernel changed "
+                       "since the last capture): issue figures withheld")
+        return out
+    ips = float(rec["thread_instr_per_state"])
+    achieved = per_launch_states * ips / 32.0 / search_s
+    out.update({"achieved": achieved / 1e9, "frac": achieved / issue_peak, "instr_per_state": ips,
+                "traffic": rec.get("dram_bytes_per_launch"),
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of the ncu --set full capture "
+                                f"({rec.get('capture')}); algorithmic HBM bytes per state: 0",
+                "record": {k: rec.get(k) for k in ("capture", "issue_active_pct", "states", "workload")}})
+    return out
 
 
 def parse():
@@ -81,6 +168,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the informational A-D config lines")
+    ap.add_argument("--shared-device", action="store_true",
+                    help="functional test of the N>1 path on fewer GPUs: ranks share devices, gloo collective "
+                         "(not a scaling measurement)")
     return ap.parse_args()
 
 
@@ -146,8 +236,11 @@ def dist_setup(gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch
 
-    if torch.cuda.is_available():
-        local = local % max(1, torch.cuda.device_count())
+    if torch.cuda.is_available() and local >= torch.cuda.device_count():
+        if not os.environ.get("QB_SHARED_DEVICE"):
+            sys.exit(f"bench.py: rank {rank} has LOCAL_RANK {local} but only {torch.cuda.device_count()} CUDA "
+                     "device(s) are visible (use --shared-device for a functional run on fewer GPUs)")
+        local = local % torch.cuda.device_count()
     if world > 1:
         import torch.distributed as dist
 
@@ -182,7 +275,7 @@ def cpu_sample(coeffs, seconds: float):
         count = count2
     states = count * per_sub
     return {"value": states / dt, "unit": "states/s", "cores": threads, "kind": "port",
-            "sample": f"{count} of {1 << m} m={m} subspaces ({states:.3g} states, {dt:.1f} s) of config E via "
+            "sample": f"extrapolated from {count} of {1 << m} m={m} subspaces ({states:.3g} states, {dt:.1f} s) of config E via "
                       f"oracle/gray_oracle.c oc_solve_subspaces (reference solve_parallel restated), {threads} threads",
             "seconds": dt}
 
@@ -250,7 +343,12 @@ def run_reference(args, world, rank):
         "unit": "states/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, bench_seed(40,0))",
-        "config": {"workload": CONFIG_DESC[args.config], "n": n, "states_per_solve": 2 ** n},
+        "extrapolated": True,
+        "extrapolation": f"each step times a bounded sample ({s['sample']}, median {statistics.median(secs):.1f} s); "
+                         f"value = sampled states/s (subspaces are equal-sized, so the rate is unbiased); "
+                         "ms_per_step = the timed sample; full_solve_ms_extrapolated = 2^n states at that rate",
+        "full_solve_ms_extrapolated": 1e3 * 2 ** n / value,
+        "config": bench_config(args.config, n),
         "cpu_baseline": {"value": value, "unit": "states/s", "cores": s["cores"], "kind": "port",
                          "sample": s["sample"]},
         "e2e": {"value": value, "unit": "states/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -258,8 +356,45 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def bench_config(name: str, n: int) -> dict:
+    """The workload description, identical in both arms (the driver compares them)."""
+    return {"workload": CONFIG_DESC[name], "n": n, "states_per_solve": 2 ** n,
+            "l2": "GPU arm: 256 MiB buffer written between timed steps (> 126 MB L2); CPU arm: host caches, no flush"}
+
+
+def self_launch(args) -> None:
+    """``--gpus N`` (N > 1) outside torchrun: re-launch this command as N ranks (one per GPU, NCCL,
+    127.0.0.1 rendezvous) -- the driver's torchrun form -- after checking that N devices exist."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    env = dict(os.environ)
+    if have < args.gpus:
+        if not args.shared_device:
+            sys.exit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible; a multi-GPU number needs "
+                     f"{args.gpus} GPUs (--shared-device runs the {args.gpus} ranks on the visible devices over "
+                     "gloo as a functional test, not a scaling measurement)")
+    if args.shared_device:
+        env["QB_SHARED_DEVICE"] = "1"
+        env["QB_DIST_BACKEND"] = "gloo"
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show nranks = N
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        self_launch(args)
+    if args.shared_device:
+        os.environ["QB_SHARED_DEVICE"] = "1"
+        os.environ.setdefault("QB_DIST_BACKEND", "gloo")
     world, rank, local = dist_setup(args.gpus)
     os.environ["QB_DEVICE"] = str(local)  # the library's default device follows the rank -> GPU map
     if args.impl == "reference":
@@ -341,30 +476,10 @@ def main():
     e2e_value = states * args.steps / e2e_max
     # roofline of the dominant (search) kernel: per-GPU launch = states/world states
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
-    sm_hz = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
+    sm_hz = (clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0) * 1e6
     per_launch_states = states / world
     search_s = search_ms_max * 1e-3 / args.steps
-    achieved = per_launch_states * (n + 1) / search_s
-    peak = FP32_ADD_LANES_PER_SM_CLK * sm_count * sm_hz
-    peak_src = "fallback 128 lanes/SM/clk x SMs x max SM clock"
-    try:
-        with open(ALU_PEAKS) as fh:
-            peak = float(json.load(fh)["results"]["fadd2"]["lane_ops_per_s"])
-        peak_src = "measured FP32 add-lane rate (tools/alu_peaks.cu, profiles/r01_alu_peaks.json)"
-    except (OSError, KeyError, ValueError):
-        pass
-    issue_peak = ISSUE_WARP_INSTR_PER_SM_CLK * 32 * sm_count * sm_hz
-    roofline = {
-        "bound": "alu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
-        "frac": achieved / peak, "traffic": ncu_traffic_bytes(),
-        "traffic_note": f"DRAM bytes per search launch from the committed ncu capture ({os.path.relpath(NCU_SUMMARY, ROOT)}, "
-                        "n=40): the per-chunk minima and CTA records; the algorithmic HBM traffic per state is 0",
-        "basis": f"nominal {n + 1} ops/state (SURVEY.md §8d: n-1 field adds + 1 value add + 1 min) vs the "
-                 f"{peak_src}; the coarse kernel issues ~{SASS_INSTR_PER_STATE} SASS instr/state, so frac > 1 "
-                 "measures the algorithmic saving and issue_frac (vs 4 warp-instr/SM/clk) the kernel quality",
-        "issue_frac": per_launch_states * SASS_INSTR_PER_STATE / search_s / issue_peak,
-        "search_ms_per_launch": search_s * 1e3,
-    }
+    roofline = roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, _lib.LIB_PATH)
     d2h = 48 + 8 + 8 * int(r.candidates) if not r.exact else 48
     line = {
         "metric": "QUBO states evaluated/sec (2^n / solve time)",
@@ -372,12 +487,10 @@ def main():
         "ms_per_step": kernel_ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded splitmix64 + Box-Muller, bench_seed(40,0); BASELINE config E)",
-        "config": {"workload": CONFIG_DESC[args.config], "n": n, "states_per_solve": states,
-                   "shards": world, "prefix_bits": int(r.prefix_bits), "exact_path": bool(r.exact),
-                   "scale_exp": int(r.scale_exp), "candidates": int(r.candidates),
-                   "l2": "256 MiB buffer written between timed steps",
-                   "argmin": hex(qb.bits_to_int(sol.minimizer)),
-                   "min_value": sol.value, "parallelism": f"prefix-shard x{world}"},
+        "config": bench_config(args.config, n),
+        "geometry": {"shards": world, "parallelism": f"prefix-shard x{world}", "prefix_bits": int(r.prefix_bits),
+                     "exact_path": bool(r.exact), "scale_exp": int(r.scale_exp), "candidates": int(r.candidates),
+                     "argmin": hex(qb.bits_to_int(sol.minimizer)), "min_value": sol.value},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": int(r.param_bytes) * int(r.launches),
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max * 1e3 / args.steps},
@@ -396,7 +509,7 @@ def main():
             vr = _lib.solve(inst.coeffs, variant=var)
             vs = states / (vr.search_ms * 1e-3)
             line["variants"][names[int(vr.variant)]] = {"search_ms": vr.search_ms, "states_per_s": vs,
-                                           "nominal_roofline_frac": vs * (n + 1) / peak,
+                                           "nominal_frac": roofline["nominal_frac"] * vs / (per_launch_states / search_s),
                                            "same_argmin": int(vr.argmin_bits) == int(r.argmin_bits)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_sample(inst.coeffs, args.cpu_seconds)

@@ -1,9 +1,21 @@
 """Summarise an ncu report: key metrics + per-opcode instruction mix (per state) of the top kernel.
-usage: python tools/ncu_summary.py report.ncu-rep [states]"""
-import csv, collections, io, subprocess, sys
+usage: python tools/ncu_summary.py report.ncu-rep [states] [--record WORKLOAD]
 
-rep = sys.argv[1]
-states = float(sys.argv[2]) if len(sys.argv) > 2 else 2.0 ** 40
+--record appends the kernel's figures to profiles/kernel_records.json keyed by the sha256 of the
+kernel's SASS in the in-tree libqubrute_b200.so (bench.py reads instructions/state and DRAM bytes
+from there only while the SASS still matches)."""
+import csv, collections, io, json, os, re, subprocess, sys
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+args = [a for a in sys.argv[1:]]
+record = None
+if "--record" in args:
+    i = args.index("--record")
+    record = args[i + 1]
+    del args[i:i + 2]
+rep = args[0]
+states = float(args[1]) if len(args) > 1 else 2.0 ** 40
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 h, units, v = r[0], r[1], r[2]
@@ -52,3 +64,26 @@ for row in rows[2:]:
 print(f"-- instruction mix: {tot:.4g} warp-instr, {tot * 32 / states:.3f} thread-instr/state")
 for op, nexec in by.most_common(14):
     print(f"  {op:10s} {nexec * 32 / states:.3f}/state")
+
+if record:
+    from bench import kernel_symbol, sass_sha256
+
+    name = out["Kernel Name"][0]
+    m = re.search(r"(\w+)<([\d, ]+)>", name)
+    fam, targs = m.group(1), [int(t) for t in m.group(2).split(",")]
+    lib_path = os.path.join(ROOT, "paper_2310_19373_b200", "libqubrute_b200.so")
+    sym = kernel_symbol(lib_path, fam, targs[4])
+    sha = sass_sha256(lib_path, sym)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    dram = sum(float(out[k][0]) * scale[out[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    path = os.path.join(ROOT, "profiles", "kernel_records.json")
+    recs = json.load(open(path)) if os.path.exists(path) else {}
+    recs[sha] = {"kernel": sym, "kernel_name": name, "workload": record, "states": states,
+                 "thread_instr_per_state": tot * 32 / states, "warp_instr": tot,
+                 "issue_active_pct": float(out["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
+                 "duration_ms": float(out["gpu__time_duration.sum"][0]) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+                                                                           "second": 1e3}[out["gpu__time_duration.sum"][1]],
+                 "dram_bytes_per_launch": dram, "capture": os.path.basename(rep)}
+    with open(path, "w") as fh:
+        json.dump(recs, fh, indent=1, sort_keys=True)
+    print(f"recorded {sym} sha {sha[:16]} -> {path}")
