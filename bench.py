@@ -96,12 +96,15 @@ def kernel_record(sha):
 
 
 def issue_peak_per_sm_clk():
-    """(warp-instructions issued per SM per clock, source) -- measured, else the architectural 4."""
+    """(warp-instructions issued per SM per clock, source): the highest rate any of the
+    tools/alu_peaks.py kernels sustained on this pool's B200 (per-clock with the sampled SM clock),
+    else the architectural 4 (one per SMSP per clock)."""
     try:
         with open(ALU_PEAKS) as fh:
-            rec = json.load(fh)["results"]["issue_ffma_iadd3"]
-        return float(rec["warp_instr_per_sm_clk"]), f"measured ({os.path.relpath(ALU_PEAKS, ROOT)}: FFMA+IADD3 " \
-            f"issue at {rec['sm_mhz_sampled']:.0f} MHz sampled)"
+            res = json.load(fh)["results"]
+        name, rec = max(res.items(), key=lambda kv: kv[1]["warp_instr_per_sm_clk"])
+        return float(rec["warp_instr_per_sm_clk"]), (f"measured ({os.path.relpath(ALU_PEAKS, ROOT)}: best issue rate, "
+                                                     f"'{name}' at {rec['sm_mhz_sampled']:.0f} MHz sampled)")
     except (OSError, KeyError, ValueError, TypeError):
         return ISSUE_WARP_INSTR_PER_SM_CLK, "fallback: 4 warp-instr/SM/clk (1 per SMSP per clock)"
 

@@ -42,9 +42,12 @@ VARIANT_TC = 4
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-ffp-contract=off",
+    # -ffp-contract=off: host eval_upper / batch folding keep the reference's fp64 operation order
+    # (no FMA contraction), which is what makes the reported values bit-identical
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp",
     "-shared",
 ]
+LINK_FLAGS = ["-Xcompiler", "-fopenmp"]
 
 
 class BackendError(RuntimeError):
@@ -115,6 +118,8 @@ def build(force: bool = False, verbose: bool = False, output: str | None = None,
     objdir = os.path.join(REPO_DIR, "build", "obj", os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(defines)
+    if not any("-ffp-contract=off" in f for f in compile_flags):
+        raise RuntimeError("libqubrute_b200 must be built with -ffp-contract=off (bit-exact host eval_upper)")
     procs = []
     objs = []
     for src in SOURCES:
@@ -127,7 +132,8 @@ def build(force: bool = False, verbose: bool = False, output: str | None = None,
     failed = [src for src, p in procs if p.wait() != 0]
     if failed:
         raise subprocess.CalledProcessError(1, f"nvcc {failed}")
-    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs], check=True)
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *LINK_FLAGS, "-o", out, *objs],
+                   check=True)
     return out
 
 

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -105,6 +106,8 @@ static KernelSet* find_set(int BE, int L) {
 // candidates read back together with the collect counts (one host round trip when they fit)
 constexpr int kCandPre = 1024;
 
+constexpr int kBatchPiecesMax = 8;
+
 struct Device {
   int id = -1;
   int sms = 0;
@@ -134,6 +137,14 @@ struct Device {
   size_t batch_coeffs_cap = 0;
   BatchOut* d_batch_out = nullptr;
   size_t batch_out_cap = 0;
+  // batch pipeline: pinned staging for the packed pieces and the results, a copy stream and
+  // per-piece events (H2D of piece p+1 overlaps the kernel of piece p)
+  double* h_batch_stage = nullptr;
+  size_t batch_stage_cap = 0;
+  BatchOut* h_batch_out = nullptr;
+  size_t batch_hout_cap = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t bev[3 * kBatchPiecesMax] = {};
   std::mutex mu;
 };
 
@@ -175,6 +186,18 @@ static int ensure(T** ptr, size_t* cap, size_t need) {
   *cap = 0;
   size_t n = std::max<size_t>(need, 64);
   QB_CUDA(cudaMalloc(ptr, n * sizeof(T)));
+  *cap = n;
+  return QB_OK;
+}
+
+template <typename T>
+static int ensure_host(T** ptr, size_t* cap, size_t need) {
+  if (*cap >= need && *ptr) return QB_OK;
+  if (*ptr) cudaFreeHost(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  size_t n = std::max<size_t>(need, 64);
+  QB_CUDA(cudaMallocHost(ptr, n * sizeof(T)));
   *cap = n;
   return QB_OK;
 }
@@ -803,6 +826,50 @@ static int prefix_impl(const double* coeffs, int n, int k, uint64_t c_begin, uin
 
 // ------------------------------------------------------------------ batch (config C)
 
+// Fold + pack instances [b0, b1) of a dense [count][n][n] batch into the upper-triangle format
+// (QuboInstance convention, core.py:66-72: v_ij = c_ij + c_ji for i < j, in fp64 with no
+// contraction), as fp32 when every folded value round-trips exactly, else as fp64.  Host threads
+// (OpenMP) split the instances.  Returns the format written, or -1 with *bad = the lowest instance
+// holding a non-finite coefficient.
+static int pack_batch_piece(const double* coeffs, int n, uint64_t b0, uint64_t b1, void* out, uint64_t* bad) {
+  const int ntri = n * (n + 1) / 2;
+  const long long cnt = (long long)(b1 - b0);
+  long long first_bad = LLONG_MAX;
+  int not_f32 = 0;
+  float* o32 = static_cast<float*>(out);
+#pragma omp parallel for schedule(static) reduction(min : first_bad) reduction(| : not_f32) if (cnt >= 256)
+  for (long long t = 0; t < cnt; ++t) {
+    const double* c = coeffs + (b0 + t) * (uint64_t)n * n;
+    float* o = o32 + t * ntri;
+    int p = 0;
+    for (int i = 0; i < n; ++i) {
+      const double* row = c + (size_t)i * n;
+      for (int j = i; j < n; ++j, ++p) {
+        const double v = (j == i) ? row[i] : row[j] + c[(size_t)j * n + i];
+        if (!std::isfinite(row[j]) || !std::isfinite(c[(size_t)j * n + i])) first_bad = std::min(first_bad, (long long)(b0 + t));
+        const float f = (float)v;
+        not_f32 |= ((double)f != v);
+        o[p] = f;
+      }
+    }
+  }
+  if (first_bad != LLONG_MAX) {
+    *bad = (uint64_t)first_bad;
+    return -1;
+  }
+  if (!not_f32) return BATCH_UPPER_F32;
+  double* o64 = static_cast<double*>(out);
+#pragma omp parallel for schedule(static) if (cnt >= 256)
+  for (long long t = 0; t < cnt; ++t) {
+    const double* c = coeffs + (b0 + t) * (uint64_t)n * n;
+    double* o = o64 + t * ntri;
+    int p = 0;
+    for (int i = 0; i < n; ++i)
+      for (int j = i; j < n; ++j, ++p) o[p] = (j == i) ? c[(size_t)i * n + i] : c[(size_t)i * n + j] + c[(size_t)j * n + i];
+  }
+  return BATCH_UPPER_F64;
+}
+
 static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                       double* kernel_ms) {
   if (!coeffs || !argmin_bits || !values) return fail(QB_E_ARG, "null pointer");
@@ -810,35 +877,65 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
   if (n > BATCH_NMAX) return fail(QB_E_CAP, "batch path supports n <= " + std::to_string(BATCH_NMAX));
   if (count == 0) return QB_OK;
   if (count > (1ull << 31) - 1) return fail(QB_E_ARG, "count too large");
-  // finiteness is checked by the kernel, which reads every coefficient anyway (status 3)
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
   std::vector<uint64_t> fallback;
   {
     std::lock_guard<std::mutex> guard(dev->mu);
-    const size_t nc = (size_t)count * n * n;
-    if (int rc = ensure(&dev->d_batch_coeffs, &dev->batch_coeffs_cap, nc)) return rc;
+    const size_t ntri = (size_t)n * (n + 1) / 2;
+    // pieces: the host packs piece p+1 while piece p is copied and solved
+    const int P = count >= 2048 ? 4 : (count >= 512 ? 2 : 1);
+    const uint64_t per = (count + P - 1) / P;
+    const size_t stage_doubles = (size_t)count * ntri;  // room for fp64 in every piece
+    if (int rc = ensure(&dev->d_batch_coeffs, &dev->batch_coeffs_cap, stage_doubles)) return rc;
+    if (int rc = ensure_host(&dev->h_batch_stage, &dev->batch_stage_cap, stage_doubles)) return rc;
     if (int rc = ensure(&dev->d_batch_out, &dev->batch_out_cap, (size_t)count)) return rc;
-    cudaStream_t st = dev->stream;
-    QB_CUDA(cudaMemcpyAsync(dev->d_batch_coeffs, coeffs, nc * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (int rc = ensure_host(&dev->h_batch_out, &dev->batch_hout_cap, (size_t)count)) return rc;
+    if (!dev->copy_stream) {
+      QB_CUDA(cudaStreamCreateWithFlags(&dev->copy_stream, cudaStreamNonBlocking));
+      for (auto& e : dev->bev) QB_CUDA(cudaEventCreate(&e));
+    }
+    cudaStream_t st = dev->stream, cs = dev->copy_stream;
     const int B = std::min(n, BMAX);
     const unsigned chunks = 1u << (n - B);
     int threads = (int)std::min<unsigned>(BATCH_TPB_MAX, std::max<unsigned>(32u, chunks));
     threads = (threads + 31) / 32 * 32;
-    BatchParams bp{dev->d_batch_coeffs, dev->d_batch_out, n, (int)count};
-    QB_CUDA(cudaEventRecord(dev->ev0, st));
     int nb = 0;
     const BatchFn* batch = batch_fns(&nb);
     if (B >= nb || !batch[B]) return fail(QB_E_INTERNAL, "no batch kernel for B=" + std::to_string(B));
-    batch[B]<<<(unsigned)count, threads, 0, st>>>(bp);
-    QB_CUDA(cudaGetLastError());
-    QB_CUDA(cudaEventRecord(dev->ev1, st));
-    std::vector<BatchOut> out(count);
-    QB_CUDA(cudaMemcpyAsync(out.data(), dev->d_batch_out, count * sizeof(BatchOut), cudaMemcpyDeviceToHost, st));
+    int pieces = 0;
+    for (int p = 0; p < P; ++p, ++pieces) {
+      const uint64_t b0 = p * per, b1 = std::min<uint64_t>(count, b0 + per);
+      if (b0 >= b1) break;
+      double* hs = dev->h_batch_stage + b0 * ntri;
+      double* ds = dev->d_batch_coeffs + b0 * ntri;
+      uint64_t bad = 0;
+      const int fmt = pack_batch_piece(coeffs, n, b0, b1, hs, &bad);
+      if (fmt < 0) {
+        cudaStreamSynchronize(st);
+        return fail(QB_E_ARG, "coefficients must be finite (instance " + std::to_string(bad) + ")");
+      }
+      const size_t bytes = (b1 - b0) * ntri * (fmt == BATCH_UPPER_F32 ? sizeof(float) : sizeof(double));
+      cudaEvent_t copied = dev->bev[3 * p], k0 = dev->bev[3 * p + 1], k1 = dev->bev[3 * p + 2];
+      QB_CUDA(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, cs));
+      QB_CUDA(cudaEventRecord(copied, cs));
+      QB_CUDA(cudaStreamWaitEvent(st, copied, 0));
+      BatchParams bp{ds, dev->d_batch_out + b0, n, (int)(b1 - b0), fmt};
+      QB_CUDA(cudaEventRecord(k0, st));
+      batch[B]<<<(unsigned)(b1 - b0), threads, 0, st>>>(bp);
+      QB_CUDA(cudaGetLastError());
+      QB_CUDA(cudaEventRecord(k1, st));
+    }
+    QB_CUDA(cudaMemcpyAsync(dev->h_batch_out, dev->d_batch_out, count * sizeof(BatchOut), cudaMemcpyDeviceToHost, st));
     QB_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    QB_CUDA(cudaEventElapsedTime(&ms, dev->ev0, dev->ev1));
-    if (kernel_ms) *kernel_ms = ms;
+    double total = 0.0;
+    for (int p = 0; p < pieces; ++p) {
+      float ms = 0.f;
+      QB_CUDA(cudaEventElapsedTime(&ms, dev->bev[3 * p + 1], dev->bev[3 * p + 2]));
+      total += ms;
+    }
+    if (kernel_ms) *kernel_ms = total;
+    const BatchOut* out = dev->h_batch_out;
     for (uint64_t b = 0; b < count; ++b) {
       if (out[b].status == 0) {
         argmin_bits[b] = out[b].x;

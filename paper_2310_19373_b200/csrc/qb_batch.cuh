@@ -103,20 +103,36 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   __shared__ Rec sbest;
   const int n = bp.n;
   const int tid = threadIdx.x, nth = blockDim.x;
-  const double* C = bp.coeffs + (size_t)blockIdx.x * n * n;
+  const int ntri = n * (n + 1) / 2;
   const int lane = tid & 31, warp = tid >> 5;
 
-  // ---- 0. fold (QuboInstance convention, core.py:66-72) into shared memory: one pass over global
+  // ---- 0. load (folded by the host for the packed formats; folded here for the dense one) into
+  //         shared memory: one pass over global memory
   if (tid == 0) { sflag[0] = sflag[1] = sflag[2] = 0; scount = 0; schunks = 0; }
   __syncthreads();
-  for (int idx = tid; idx < n * n; idx += nth) {
-    const int i = idx / n, j = idx % n;
-    if (j < i) continue;
-    const double a = C[idx], b = (i == j) ? 0.0 : C[j * n + i];
-    if (!isfinite(a) || !isfinite(b)) sflag[2] = 1;  // reported to the host as QB_E_ARG
-    const double v = (i == j) ? a : __dadd_rn(a, b);
-    sC[i][j] = v;
-    sC[j][i] = v;
+  if (bp.fmt == BATCH_DENSE_F64) {
+    const double* C = static_cast<const double*>(bp.coeffs) + (size_t)blockIdx.x * n * n;
+    for (int idx = tid; idx < n * n; idx += nth) {
+      const int i = idx / n, j = idx % n;
+      if (j < i) continue;
+      const double a = C[idx], b = (i == j) ? 0.0 : C[j * n + i];
+      if (!isfinite(a) || !isfinite(b)) sflag[2] = 1;  // reported to the host as QB_E_ARG
+      const double v = (i == j) ? a : __dadd_rn(a, b);
+      sC[i][j] = v;
+      sC[j][i] = v;
+    }
+  } else {
+    for (int p = tid; p < ntri; p += nth) {
+      // row i of the packed upper triangle starts at i*n - i*(i-1)/2
+      int i = 0;
+      while ((i + 1) * n - (i + 1) * i / 2 <= p) ++i;
+      const int j = i + (p - (i * n - i * (i - 1) / 2));
+      const double v = bp.fmt == BATCH_UPPER_F32 ? (double)static_cast<const float*>(bp.coeffs)[(size_t)blockIdx.x * ntri + p]
+                                                 : static_cast<const double*>(bp.coeffs)[(size_t)blockIdx.x * ntri + p];
+      if (!isfinite(v)) sflag[2] = 1;
+      sC[i][j] = v;
+      sC[j][i] = v;
+    }
   }
   __syncthreads();
   if (sflag[2]) {  // every coefficient is read here, so the host needs no pass over the batch

@@ -14,11 +14,18 @@ struct BatchOut {
   int candidates;
 };
 
+// Input formats of the batch kernel.  The host folds each instance (QuboInstance convention,
+// core.py:66-72) and packs its upper triangle row by row (i <= j), as fp32 when every folded
+// coefficient of the piece round-trips through fp32 exactly (config C: 4x fewer H2D bytes than the
+// dense fp64 matrix), otherwise as fp64.
+enum BatchFmt : int { BATCH_DENSE_F64 = 0, BATCH_UPPER_F32 = 1, BATCH_UPPER_F64 = 2 };
+
 struct BatchParams {
-  const double* coeffs;  // [count][n][n] fp64; entries below the diagonal are folded in
-  BatchOut* out;         // [count]
+  const void* coeffs;  // [count] instances in format `fmt`
+  BatchOut* out;       // [count]
   int n;
   int count;
+  int fmt;             // BatchFmt
 };
 
 }  // namespace qb

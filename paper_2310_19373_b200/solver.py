@@ -232,7 +232,9 @@ def solve_batch(instances, *, as_arrays: bool = False):
         return (np.zeros((0, n), dtype=np.uint8), np.zeros(0)) if as_arrays else []
     t0 = time.perf_counter()
     bits, vals, _ = _lib.solve_batch(coeffs)
-    minimizers = ((bits[:, None] >> np.arange(n, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.uint8)
+    # bit i of each little-endian uint64 -> column i (one vectorised pass, no per-bit shifts)
+    minimizers = np.unpackbits(bits.astype("<u8").view(np.uint8).reshape(count, 8), axis=1,
+                               bitorder="little")[:, :n]
     if as_arrays:
         return minimizers, vals
     elapsed = max(time.perf_counter() - t0, 1e-9)

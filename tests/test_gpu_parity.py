@@ -252,6 +252,31 @@ def test_batch_float_instances_vs_oracle():
         assert vals.tolist() == ov.tolist()
 
 
+def test_batch_pipeline_mixed_formats_and_folding():
+    """The host packs the batch in pieces (fp32 upper triangle when every folded coefficient is
+    fp32-exact, else fp64) and pipelines pack / H2D / kernel.  3000 instances = 4 pieces; one
+    piece holds a coefficient that is not fp32-representable (that piece ships fp64), and half of
+    the instances carry their off-diagonal weights split between the upper and lower triangle, so
+    the host fold (core.py:66-72) is exercised.  Every answer equals the oracle on the folded
+    matrices, bit for bit."""
+    n, count = 14, 3000
+    batch = np.stack([instances.normal_coeffs(n, 9100 + b, density=0.5) for b in range(count)])
+    iu = np.triu_indices(n, 1)
+    for b in range(0, count, 2):
+        half = np.float32(0.5) * batch[b][iu].astype(np.float32)
+        batch[b][(iu[1], iu[0])] = half
+        batch[b][iu] = batch[b][iu] - half
+    batch[1700, 2, 5] += 0.1  # piece 2 (instances 1500..2249) -> fp64 format
+    folded = np.stack([qb.QuboInstance(batch[b]).coeffs for b in range(count)])
+    bits, vals, _ = _lib.solve_batch(batch)
+    ob, ov = O.solve_batch(folded, threads=8)
+    assert [int(b) for b in bits] == [int(b) for b in ob]
+    assert vals.tolist() == ov.tolist()
+    mins, mvals = qb.solve_batch(batch, as_arrays=True)
+    assert mins.shape == (count, n) and mins.dtype == np.uint8
+    assert [qb.bits_to_int(mins[b]) for b in range(0, count, 97)] == [int(ob[b]) for b in range(0, count, 97)]
+
+
 @pytest.mark.parametrize("n,k", [(24, 14), (30, 14), (22, 12), (18, 9)])
 def test_prefix_eval_hook(n, k):
     c = instances.config_coeffs("D", 2, n=n)

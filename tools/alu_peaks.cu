@@ -38,7 +38,7 @@ __device__ __forceinline__ long long clk() {
 enum { K_FADD, K_FADD2, K_FFMA, K_FMNMX3, K_DADD, K_IADD3, K_VIMNMX3, K_MIX, K_VIADD16, K_VMIN3_16, K_MIX16, K_ISSUE, K_NK };
 static const char* NAMES[K_NK] = {"fadd", "fadd2", "ffma", "fmnmx3", "dadd", "iadd3", "vimnmx3",
                                   "mix_fadd2_fmnmx3_ldcu128", "viadd_16x2", "vimnmx3_s16x2",
-                                  "mix16_viadd2_vimnmx3_ldcu128", "issue_ffma_iadd3"};
+                                  "mix16_viadd2_vimnmx3_ldcu128", "issue_fadd_iadd3"};
 // lane-operations per instruction: FADD2 / IADD3 = 2 adds, FMNMX3 / VIMNMX3 = 2 two-input mins,
 // MIX counts states (one FADD2 + one FMNMX3 per 2 states)
 static const double OPS[K_NK] = {1, 2, 1, 2, 1, 2, 2, 2, 2, 4, 2, 1};
@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(TPB, 2) kern(const __grid_constant__ Tab tab, 
 #pragma unroll
     for (int i = 0; i < CH; i++) acc += (float)(v[i] & 0xffff);
   } else if constexpr (K == K_ISSUE) {
-    // issue-slot peak: every iteration issues one FFMA (FMA pipe) and one IADD3 (ALU pipe) per chain,
-    // independent pipes at rt_SMSP = 2 each, so the SMSP can issue one instruction per clock
+    // issue-slot peak: every iteration issues one FADD (FMA pipes) and one IADD3 (ALU pipe) per chain,
+    // independent pipes, so the SMSP can issue up to one instruction per clock
     float f[CH];
     int v[CH];
 #pragma unroll
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(TPB, 2) kern(const __grid_constant__ Tab tab, 
     for (int it = 0; it < ITERS; it++) {
 #pragma unroll
       for (int i = 0; i < CH; i++) {
-        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(f[(i + 1) % CH]), "f"(f[(i + 3) % CH]));
+        asm volatile("add.rn.f32 %0, %0, %1;" : "+f"(f[i]) : "f"(f[(i + 1) % CH]));
         asm volatile("{ .reg .s32 t; add.s32 t, %0, %1; add.s32 %0, t, %2; }" : "+r"(v[i]) : "r"(v[(i + 1) % CH]), "r"(v[(i + 2) % CH]));
       }
     }

@@ -26,7 +26,7 @@ from bench import ClockSampler  # noqa: E402
 BIN = os.path.join(ROOT, "tools", "alu_peaks")
 SRC = BIN + ".cu"
 NAMES = ["fadd", "fadd2", "ffma", "fmnmx3", "dadd", "iadd3", "vimnmx3", "mix_fadd2_fmnmx3_ldcu128", "viadd_16x2",
-         "vimnmx3_s16x2", "mix16_viadd2_vimnmx3_ldcu128", "issue_ffma_iadd3"]
+         "vimnmx3_s16x2", "mix16_viadd2_vimnmx3_ldcu128", "issue_fadd_iadd3"]
 
 
 def main() -> None:

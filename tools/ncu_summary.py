@@ -81,7 +81,7 @@ if record:
     recs[sha] = {"kernel": sym, "kernel_name": name, "workload": record, "states": states,
                  "thread_instr_per_state": tot * 32 / states, "warp_instr": tot,
                  "issue_active_pct": float(out["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
-                 "duration_ms": float(out["gpu__time_duration.sum"][0]) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+                 "duration_ms": float(out["gpu__time_duration.sum"][0]) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3,
                                                                            "second": 1e3}[out["gpu__time_duration.sum"][1]],
                  "dram_bytes_per_launch": dram, "capture": os.path.basename(rep)}
     with open(path, "w") as fh:
