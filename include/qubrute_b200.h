@@ -47,6 +47,8 @@ extern "C" {
 #define QB_VARIANT_FIELDWALK 2 /* per-step Gray walk with register local fields (Alg. 1 form) */
 #define QB_VARIANT_COARSE 3    /* table walk with a packed-int16 block pass + exact re-evaluation */
 #define QB_VARIANT_TC 4        /* coarse block pass formed by tcgen05.mma (f16, TMEM) + exact re-evaluation */
+#define QB_VARIANT_IMM 5       /* coarse kernel with the instance's coarse table patched into its SASS as
+                                  instruction immediates (no table loads); AUTO's choice where COARSE runs */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {
@@ -136,6 +138,11 @@ int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin
  * eval_upper / delta (core.py:123-150). */
 int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_t count, double* values,
                    double* fields);
+
+/* Test hook (host only): the embedded patched-immediate cubin for chunk length L with the 512 coarse
+ * table words `words` written into its placeholder immediates -- the image QB_VARIANT_IMM loads.
+ * *size receives the image size; the image is copied to `out` when cap >= *size. */
+int qb_imm_image(int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,9 @@ HEADER = os.path.join(REPO_DIR, "include", "qubrute_b200.h")
 SOURCES = [os.path.join(PKG_DIR, "csrc", f)
            for f in ("qb_api.cu", "qb_k_table.cu", "qb_k_coarse.cu", "qb_k_fieldwalk.cu", "qb_k_batch.cu", "qb_k_tc.cu")]
 DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]
+# patched-immediate coarse kernels (QB_VARIANT_IMM): one cubin per chunk length, embedded in the .so
+IMM_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse_imm.cu")
+IMM_LS = (10, 11, 12, 13, 14, 16, 18, 20, 22)
 
 QB_OK = 0
 QB_E_ARG = -1
@@ -38,6 +41,7 @@ VARIANT_TABLE = 1
 VARIANT_FIELDWALK = 2
 VARIANT_COARSE = 3
 VARIANT_TC = 4
+VARIANT_IMM = 5
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -98,6 +102,8 @@ SIGNATURES = {
                                     _u64p]),
     "qb_solve_batch": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, _u64p, _dp, _dp]),
     "qb_prefix_eval": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _dp, _dp]),
+    "qb_imm_image": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.c_char_p, ctypes.c_uint64,
+                                    _u64p]),
 }
 
 _lock = threading.Lock()
@@ -129,12 +135,43 @@ def build(force: bool = False, verbose: bool = False, output: str | None = None,
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
+    cubins = []
+    for L in IMM_LS:
+        cub = os.path.join(objdir, f"qb_coarse_imm_L{L}.cubin")
+        cmd = ["nvcc", *[f for f in compile_flags if not f.startswith("-Xcompiler") and "-fPIC" not in f],
+               f"-DQB_IMM_L={L}", "-cubin", "-o", cub, IMM_SOURCE]
+        procs.append((f"{IMM_SOURCE} (L={L})", subprocess.Popen(cmd)))
+        cubins.append((L, cub))
     failed = [src for src, p in procs if p.wait() != 0]
     if failed:
         raise subprocess.CalledProcessError(1, f"nvcc {failed}")
+    objs.append(_embed_cubins(objdir, cubins))
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *LINK_FLAGS, "-o", out, *objs],
                    check=True)
     return out
+
+
+def _embed_cubins(objdir: str, cubins) -> str:
+    """C object holding the patched-immediate cubins as byte arrays (qb_imm_cubins[], read by
+    qb_api.cu imm_module), compiled with the host C compiler."""
+    csrc = os.path.join(objdir, "qb_imm_cubins.c")
+    with open(csrc, "w") as fh:
+        fh.write("/* generated by paper_2310_19373_b200/_lib.py: patched-immediate coarse cubins */\n")
+        fh.write("#include <stddef.h>\n")
+        for L, path in cubins:
+            data = open(path, "rb").read()
+            fh.write(f"static const unsigned char cubin_L{L}[{len(data)}] __attribute__((aligned(16))) = {{\n")
+            for i in range(0, len(data), 32):
+                fh.write(",".join(str(b) for b in data[i:i + 32]) + ",\n")
+            fh.write("};\n")
+        fh.write("struct qb_imm_cubin { int L; const unsigned char* data; size_t size; };\n")
+        fh.write("const struct qb_imm_cubin qb_imm_cubins[] = {\n")
+        for L, path in cubins:
+            fh.write(f"  {{{L}, cubin_L{L}, sizeof(cubin_L{L})}},\n")
+        fh.write("  {0, 0, 0}};\n")
+    obj = csrc.replace(".c", ".o")
+    subprocess.run(["cc", "-O1", "-fPIC", "-c", "-o", obj, csrc], check=True)
+    return obj
 
 
 def lib():
@@ -277,3 +314,16 @@ def prefix_eval(coeffs, k: int, c_begin: int, count: int, device: int | None = N
     rc = lib().qb_prefix_eval(_ptr(c), n, k, c_begin, count, _ptr(vals), _ptr(fields))
     check(rc, "qb_prefix_eval")
     return vals, fields
+
+
+def imm_image(L: int, words) -> bytes:
+    """The patched-immediate cubin for chunk length L with coarse table words `words` (test hook)."""
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    if w.shape != (512,):
+        raise ValueError("need 512 table words")
+    size = ctypes.c_uint64()
+    wp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+    check(lib().qb_imm_image(L, wp, None, 0, ctypes.byref(size)), "qb_imm_image")
+    buf = ctypes.create_string_buffer(size.value)
+    check(lib().qb_imm_image(L, wp, buf, size.value, ctypes.byref(size)), "qb_imm_image")
+    return buf.raw[: size.value]

@@ -61,8 +61,19 @@ __device__ __forceinline__ unsigned umin2(unsigned a, unsigned b) {
 }
 __device__ __forceinline__ unsigned umin3(unsigned a, unsigned b, unsigned c) { return umin2(umin2(a, b), c); }
 
+// a + imm on the FMA pipe (IMAD with an opaque multiplier of 1): the pass splits its adds between
+// the FMA pipe (this) and the ALU pipe (fused VIADDMNMX) so neither pipe limits the issue rate
+__device__ __forceinline__ unsigned add_fma_pipe(unsigned a, unsigned one, unsigned imm) {
+  unsigned r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(imm));
+  return r;
+}
+
 // Coarse minimum over the 2^B states of a block, in coarse units (exact integer arithmetic).
-template <int B1, int B2>
+// IMM: the table words are instruction immediates (patched per instance) instead of constant-bank
+// loads; per row of 32 pairs, 22 pairs are formed by IMAD (FMA pipe) and folded by VIMNMX3, 10 by
+// the fused VIADDMNMX (ALU pipe): ~0.71 issue slots per state, both pipes ~equally loaded.
+template <int B1, int B2, bool IMM = false>
 __device__ __forceinline__ int coarse_block_min(const TableParams& p, const float (&H)[B1 + B2]) {
   constexpr int B = B1 + B2, NU = 1 << B1, NP = 1 << (B2 - 1);
   static_assert(B2 >= 3, "pairs of w, four pairs per table load");
@@ -90,6 +101,34 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
     for (int u = 0; u < (1 << i); ++u) A2[u + (1 << i)] = A2[u] + d;
   }
   unsigned rmin2 = 0u;
+  if constexpr (IMM) {
+    const unsigned one = p.imm_one;
+#pragma unroll
+    for (int u = 0; u < NU; u += 2) {
+      unsigned r2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const unsigned ph = QB_IMM_PH | (unsigned)((u + h) * NP);
+        unsigned acc = 0u, f0 = 0xffffffffu, f1 = 0xffffffffu;
+#pragma unroll
+        for (int m = 0; m < NP; m += 3) {
+          if (m + 1 < NP) {
+            const unsigned c0 = add_fma_pipe(Bw2[m], one, ph | m), c1 = add_fma_pipe(Bw2[m + 1], one, ph | (m + 1));
+            acc = (m == 0) ? umin2(c0, c1) : umin3(acc, c0, c1);
+          }
+          if (m + 2 < NP) {
+            if ((m / 3) & 1)
+              f1 = __viaddmin_u16x2(Bw2[m + 2], ph | (m + 2), f1);
+            else
+              f0 = __viaddmin_u16x2(Bw2[m + 2], ph | (m + 2), f0);
+          }
+        }
+        r2[h] = umin3(acc, f0, f1) + A2[u + h];
+      }
+      rmin2 = (u == 0) ? umin2(r2[0], r2[1]) : umin3(rmin2, r2[0], r2[1]);
+    }
+    return (int)min(rmin2 & 0xffffu, rmin2 >> 16) - 4 * CB;
+  } else {
 #pragma unroll
   for (int u = 0; u < NU; u += 2) {
     unsigned r2[2];
@@ -125,7 +164,8 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
     }
     rmin2 = (u == 0) ? umin2(r2[0], r2[1]) : umin3(rmin2, r2[0], r2[1]);
   }
-  const int rmin = (int)min(rmin2 & 0xffffu, rmin2 >> 16) - 4 * CB;
+  return (int)min(rmin2 & 0xffffu, rmin2 >> 16) - 4 * CB;
+  }
 #else
   // A[u] = sum_{i in u} hc_{B2+i} - 2^15 (removes the two field biases of a candidate)
   int A[NU];
@@ -153,8 +193,8 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
     }
     rmin = (u == 0) ? min(r[0], r[1]) : min(min(rmin, r[0]), r[1]);
   }
-#endif
   return rmin;
+#endif
 }
 
 // (B1, B2): the fp32 table split used by the exact fallback; (CB1, CB2): the coarse pass's own split
@@ -180,7 +220,7 @@ __device__ __noinline__ ChunkStart<B, ((L - B) > 0 ? (L - B) : 1)> chunk_start_o
   return r;
 }
 
-template <int B1, int B2, int CB1, int CB2, int L, int TPB>
+template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool IMM = false>
 __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(CB1 + CB2 == B, "coarse split must cover the table bits");
@@ -236,7 +276,7 @@ __global__ void __launch_bounds__(TPB, QB_COARSE_MINB) coarse_kernel(const __gri
       // the chunk start (measured: the per-block load costs ~5% at 1024 blocks per chunk)
       long long gb = LLONG_MAX;
       if constexpr (LO <= 6) gb = gbest_dec(__ldcg(p.gbest));
-      const long long cb = V + ((long long)coarse_block_min<CB1, CB2>(p, H) << p.coarse_shift);
+      const long long cb = V + ((long long)coarse_block_min<CB1, CB2, IMM>(p, H) << p.coarse_shift);
       if constexpr (LO <= 6) {
         thr = min(thr, gb);
         lim = thr > LLONG_MAX - slack ? LLONG_MAX : thr + slack;

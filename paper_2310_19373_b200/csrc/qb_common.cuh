@@ -25,6 +25,12 @@ namespace qb {
 constexpr int NMAX = 40;   // reference core.py:24 MAX_DIM
 constexpr int BMAX = 10;   // largest inner block (1024-entry table, 4 KB in the constant bank)
 
+// Placeholder immediates of the patched-immediate coarse pass (QB_VARIANT_IMM, qb_coarse.cuh):
+// table word Tc2[u * NP + m] appears in the SASS as the 32-bit immediate QB_IMM_PH | (u * NP + m)
+// and is replaced by the instance's word in a copy of the cubin before it is loaded (qb_api.cu,
+// imm_kernel).  The adds then need no table load at all (no LDCU / LDC).
+constexpr unsigned QB_IMM_PH = 0x7A5C0000u;
+
 // tensor-core coarse pass (qb_tc.cuh): two states per TMEM cell, K = 32 f16 operands
 constexpr int TC_WORKERS = 128;                // worker threads = rows of one MMA
 constexpr int TC_TPB = TC_WORKERS + 32;        // + the MMA issuer warp
@@ -71,6 +77,7 @@ struct alignas(16) TableParams {
   float coarse_scale;        // 2^-s: coarse units per quantized unit
   int coarse_shift;          // s (coarse unit = 2^s quantized units); 0 = coarse is exact
   long long seed_val;        // quantized value of a state found by host greedy descent (LLONG_MAX: none)
+  unsigned imm_one;          // 1, opaque to ptxas (the patched-immediate coarse pass's FMA-pipe adds)
   float tc_scale;            // tensor-core pass (qb_tc.cuh): 2^-s_tc
   int tc_shift;              // s_tc: f16 coarse unit = 2^s_tc quantized units; 0 = exact
   int tc_bias;               // beta: added to every coarse table entry so all f16 results are >= 0

@@ -1,0 +1,81 @@
+"""GPU parity of the patched-immediate coarse kernel (QB_VARIANT_IMM, AUTO's default where the coarse
+filter runs): the instance's coarse table is written into the kernel's SASS as instruction immediates
+(qb_api.cu imm_kernel / imm_patch).  Every result must equal the table-load coarse kernel's (same
+blocks, same certified bounds, same tie keys) and, where affordable, the oracle's."""
+
+import numpy as np
+import pytest
+
+import paper_2310_19373_b200 as qb
+from oracle import oracle as O
+from paper_2310_19373_b200 import _lib, instances
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(a, b):
+    return (int(a.argmin_bits), a.value, int(a.tie_key), int(a.value_key)) == \
+        (int(b.argmin_bits), b.value, int(b.tie_key), int(b.value_key))
+
+
+CASES = [("E", 40, 0), ("E", 40, 1), ("E", 36, 2), ("E", 33, 3), ("D", 32, 0), ("D", 32, 4), ("B", 31, 1),
+         ("B", 34, 2), ("A", 32, 5)]
+
+
+@pytest.mark.parametrize("name,n,rep", CASES)
+def test_imm_equals_table_load_coarse(name, n, rep):
+    c = instances.config_coeffs(name, rep, n=n)
+    ref = _lib.solve(c, variant=_lib.VARIANT_COARSE)
+    got = _lib.solve(c, variant=_lib.VARIANT_IMM)
+    assert got.variant == _lib.VARIANT_IMM and ref.variant == _lib.VARIANT_COARSE
+    assert _same(got, ref), (name, n, rep)
+    auto = _lib.solve(c)
+    assert auto.variant == _lib.VARIANT_IMM and _same(auto, ref)
+
+
+@pytest.mark.parametrize("m_fix,m_tie,shards", [(0, 6, 1), (0, 0, 3), (4, 4, 1), (2, 9, 2)])
+def test_imm_subspaces_ties_and_shards(m_fix, m_tie, shards):
+    """Tie-heavy integer instance (values in {-1,0,1}): subspace solves, the parallel tie rule and
+    shards all agree between the two coarse kernels."""
+    c = instances.int_uniform_coeffs(33, 777, -1, 1)
+    for shard in range(shards):
+        suffix = 3 if m_fix else 0
+        ref = _lib.solve(c, m_fix, suffix, m_tie, shard=shard, shard_count=shards, variant=_lib.VARIANT_COARSE)
+        got = _lib.solve(c, m_fix, suffix, m_tie, shard=shard, shard_count=shards, variant=_lib.VARIANT_IMM)
+        assert _same(got, ref), (m_fix, m_tie, shard)
+
+
+def test_imm_module_cache_alternating_instances():
+    """More distinct instances than the per-device module cache holds (4), solved twice in
+    alternating order: every answer is the one of its own instance (cache keyed by table + L)."""
+    cs = [instances.config_coeffs("E", 10 + r, n=32) for r in range(6)]
+    want = [_lib.solve(c, variant=_lib.VARIANT_COARSE) for c in cs]
+    for _ in range(2):
+        for c, w in zip(cs, want):
+            assert _same(_lib.solve(c, variant=_lib.VARIANT_IMM), w)
+
+
+def test_imm_vs_oracle_subspace_n34():
+    """Oracle check of an IMM search on a float instance: solve_subspace over 2^26 states."""
+    c = instances.config_coeffs("E", 7, n=34)
+    m, suffix = 8, 77
+    got = _lib.solve(c, m, suffix, m, variant=_lib.VARIANT_IMM)
+    assert got.variant == _lib.VARIANT_IMM
+    bits, val, _ = O.solve_subspaces(c, m, suffix, suffix + 1, threads=8)
+    assert int(got.argmin_bits) == bits and got.value == val
+
+
+def test_imm_adversarial_ranges():
+    """Wide-range weights (one huge term, many tiny non-integer ones) and an all-zero instance."""
+    n = 32
+    c = np.zeros((n, n))
+    c[0, 0] = -1.0e9
+    rng = np.random.default_rng(5)
+    iu = np.triu_indices(n, 1)
+    c[iu] = rng.standard_normal(len(iu[0])) * 1e-3
+    inst = qb.QuboInstance(c)
+    ref = _lib.solve(inst.coeffs, variant=_lib.VARIANT_COARSE)
+    got = _lib.solve(inst.coeffs, variant=_lib.VARIANT_IMM)
+    assert _same(got, ref)
+    z = np.zeros((n, n))
+    assert _same(_lib.solve(z, variant=_lib.VARIANT_IMM), _lib.solve(z, variant=_lib.VARIANT_COARSE))
