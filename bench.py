@@ -62,7 +62,7 @@ def kernel_symbol(lib_path: str, family: str, L: int):
                              timeout=60).stdout
     except (OSError, subprocess.SubprocessError):
         return None
-    pat = re.compile(r"_ZN2qb%d%sI(?:Li\d+E){4}Li%dE(?:Li\d+E)*EEvNS_\w+E$" % (len(family), family, L))
+    pat = re.compile(r"_ZN2qb%d%sI(?:Li\d+E){4}Li%dE(?:L[ib]\d+E)*EEvNS_\w+E$" % (len(family), family, L))
     for line in out.split("\n"):
         parts = line.split()
         if parts and pat.match(parts[-1]):
@@ -83,6 +83,29 @@ def sass_sha256(lib_path: str, symbol: str):
     if not body:
         return None
     return hashlib.sha256("\n".join(body).encode()).hexdigest()
+
+
+def imm_sass_sha256(L: int):
+    """sha256 of the SASS of the patched-immediate coarse kernel for chunk length L with its
+    placeholders in place (the code, independent of any instance's table words), or None."""
+    import tempfile
+
+    import numpy as np
+
+    from paper_2310_19373_b200 import _lib
+
+    try:
+        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(512, dtype=np.uint32))
+    except Exception:  # noqa: BLE001 - no cubin for this L / library without the IMM kernels
+        return None
+    with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
+        fh.write(img)
+        fh.flush()
+        return sass_sha256(fh.name, imm_symbol(L))
+
+
+def imm_symbol(L: int) -> str:
+    return f"_ZN2qb13coarse_kernelILi5ELi5ELi4ELi6ELi{L}ELi128ELb1EEEvNS_11TableParamsE"
 
 
 def kernel_record(sha):
@@ -118,7 +141,7 @@ def fp32_lane_peak_per_sm_clk():
         return FP32_ADD_LANES_PER_SM_CLK, "fallback 128 FP32 lanes/SM/clk"
 
 
-FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel"}
+FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel", 5: "coarse_kernel (imm)"}
 
 
 def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path):
@@ -131,8 +154,11 @@ def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path)
     state's value with ~1 instruction instead of n+1 additions."""
     L = n - int(r.prefix_bits)
     family = FAMILIES.get(int(r.variant))
-    sym = kernel_symbol(lib_path, family, L) if family else None
-    sha = sass_sha256(lib_path, sym) if sym else None
+    if int(r.variant) == 5:  # patched-immediate kernel: SASS of the embedded cubin, placeholders in place
+        sym, sha = imm_symbol(L), imm_sass_sha256(L)
+    else:
+        sym = kernel_symbol(lib_path, family, L) if family else None
+        sha = sass_sha256(lib_path, sym) if sym else None
     rec = kernel_record(sha)
     ipc, ipc_src = issue_peak_per_sm_clk()
     lanes, lanes_src = fp32_lane_peak_per_sm_clk()

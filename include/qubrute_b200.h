@@ -71,6 +71,9 @@ typedef struct qb_result {
   int32_t launches;       /* kernels launched by this call */
   int32_t grid;           /* CTAs of the traversal launch */
   uint64_t param_bytes;   /* bytes of kernel parameters copied host->device per launch (Q, T tables) */
+  double module_ms;       /* host time patching + loading the patched-immediate kernel (0: cached / not used) */
+  int32_t combine;        /* qb_solve_devices: 1 = shards combined by one ncclAllReduce, 0 = on the host */
+  int32_t reserved;
 } qb_result;
 
 /* Library / device management. */
@@ -130,6 +133,13 @@ int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, con
  * this replaces a loop / thread pool of solve_incremental calls (solver.py:118-136). */
 int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                    double* kernel_ms);
+
+/* The batch sharded over several GPUs of this process: contiguous slices
+ * of the instances, slice i solved by qb_solve_batch on devices[i] from its own host thread, results
+ * written in place (the gather is the caller's arrays).  *kernel_ms = the maximum over slices.  A
+ * device may appear more than once (its slices then run one after another). */
+int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const int* devices, int ndev,
+                           uint64_t* argmin_bits, double* values, double* kernel_ms);
 
 /* Test hook: chunk-start ("prefix") evaluation used by the traversal kernels, run as a standalone
  * kernel.  For each of `count` chunks c in [c_begin, c_begin+count) of an n-bit problem with

@@ -77,6 +77,9 @@ class QbResult(ctypes.Structure):
         ("launches", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("param_bytes", ctypes.c_uint64),
+        ("module_ms", ctypes.c_double),
+        ("combine", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -101,6 +104,8 @@ SIGNATURES = {
     "qb_gray_scan": (ctypes.c_int, [_dp, _dp, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _dp,
                                     _u64p]),
     "qb_solve_batch": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, _u64p, _dp, _dp]),
+    "qb_solve_batch_devices": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int),
+                                              ctypes.c_int, _u64p, _dp, _dp]),
     "qb_prefix_eval": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _dp, _dp]),
     "qb_imm_image": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.c_char_p, ctypes.c_uint64,
                                     _u64p]),
@@ -302,6 +307,20 @@ def solve_batch(coeffs_batch, device: int | None = None):
     ms = ctypes.c_double()
     rc = lib().qb_solve_batch(_ptr(c), n, count, bits.ctypes.data_as(_u64p), _ptr(vals), ctypes.byref(ms))
     check(rc, "qb_solve_batch")
+    return bits, vals, ms.value
+
+
+def solve_batch_devices(coeffs_batch, devices):
+    """The batch split over ``devices`` (qb_solve_batch_devices): slice i of the instances on devices[i]."""
+    c = _f64(coeffs_batch)
+    count, n = c.shape[0], c.shape[1]
+    devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+    bits = np.zeros(count, dtype=np.uint64)
+    vals = np.zeros(count)
+    ms = ctypes.c_double()
+    rc = lib().qb_solve_batch_devices(_ptr(c), n, count, devs, len(devices), bits.ctypes.data_as(_u64p), _ptr(vals),
+                                      ctypes.byref(ms))
+    check(rc, "qb_solve_batch_devices")
     return bits, vals, ms.value
 
 

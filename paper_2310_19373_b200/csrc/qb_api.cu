@@ -9,6 +9,8 @@
 // The reference's equivalents are solver.py:118-229 (dispatch, subspace fan-out, reduce)
 // and _kernels.py:12-75 (the numba kernels).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -109,6 +111,7 @@ constexpr int kCandPre = 1024;
 
 constexpr int kBatchPiecesMax = 8;
 constexpr int kImmCache = 4;
+constexpr int kImmSeen = 16;
 
 // One patched copy of a qb_coarse_imm_L<L> cubin, loaded as a CUDA library (qb_k_coarse_imm.cu).
 struct ImmModule {
@@ -159,6 +162,8 @@ struct Device {
   cudaEvent_t bev[3 * kBatchPiecesMax] = {};
   ImmModule imm[kImmCache];  // patched-immediate coarse kernels loaded on this device (LRU)
   unsigned long long imm_clock = 0;
+  unsigned long long imm_seen[kImmSeen] = {};  // table hashes solved recently (AUTO loads on a repeat)
+  unsigned imm_seen_next = 0;
   std::mutex mu;
 };
 
@@ -286,9 +291,28 @@ static std::string imm_kernel_name(int L) {
 
 // The patched kernel for chunk length L and table words tc2 on this device (cached).  Returns
 // QB_OK with *out set, or a QB_E_* code (no cubin for L, rejected image, load failure).
-static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out, bool* loaded) {
+static unsigned long long imm_hash(int L, const unsigned* tc2) {
   unsigned long long h = 1469598103934665603ull ^ (unsigned long long)L;
   for (int i = 0; i < kImmWords; ++i) h = (h ^ tc2[i]) * 1099511628211ull;
+  return h;
+}
+
+// AUTO's choice: patching + loading a module costs ~1-3 ms of host time, so a first solve only takes
+// the patched-immediate kernel when its search is long (>= QB_IMM_MIN_MS, default 16 ms of estimated
+// search); a table already loaded, or one solved before on this device, always does.
+static bool imm_auto(Device* dev, int L, unsigned long long h, double est_ms) {
+  for (auto& m : dev->imm)
+    if (m.lib && m.L == L && m.hash == h) return true;
+  bool seen = false;
+  for (unsigned long long x : dev->imm_seen) seen |= (x == h);
+  if (!seen) dev->imm_seen[dev->imm_seen_next++ % kImmSeen] = h;
+  const char* e = std::getenv("QB_IMM_MIN_MS");
+  const double min_ms = e ? std::atof(e) : 16.0;
+  return seen || est_ms >= min_ms;
+}
+
+static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out, bool* loaded) {
+  const unsigned long long h = imm_hash(L, tc2);
   *loaded = false;
   for (auto& m : dev->imm)
     if (m.lib && m.L == L && m.hash == h) {
@@ -328,6 +352,53 @@ static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out
 static bool imm_enabled() {
   const char* e = std::getenv("QB_IMM");
   return !(e && e[0] == '0');
+}
+
+// ------------------------------------------------------------------ NCCL combine (qb_solve_devices)
+// The single-process multi-GPU solve combines its shards with one ncclAllReduce(MIN) over a
+// [3 * ndev] int64 buffer (slot r of each third = shard r's value key, tie key, argmin; the other
+// slots INT64_MAX, so the MIN is an all-gather), the same exchange as distributed.py's torchrun path
+// (SURVEY.md section 8e).  libnccl is opened at run time (no link dependency; torch's copy is reused
+// when already loaded); communicators from ncclCommInitAll are cached for the last device list.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::vector<int> devs;  // device list of the cached communicators
+  std::vector<ncclComm_t> comms;
+  std::mutex mu;
+};
+static NcclApi g_nccl;
+
+static bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.comm_init_all = (decltype(g_nccl.comm_init_all))dlsym(h, "ncclCommInitAll");
+  g_nccl.all_reduce = (decltype(g_nccl.all_reduce))dlsym(h, "ncclAllReduce");
+  g_nccl.comm_destroy = (decltype(g_nccl.comm_destroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.error_string = (decltype(g_nccl.error_string))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.comm_init_all && g_nccl.all_reduce && g_nccl.comm_destroy && g_nccl.error_string;
+  return g_nccl.ok;
+}
+
+// communicators for `devs` (caller holds g_nccl.mu)
+static int nccl_comms(const std::vector<int>& devs) {
+  if (g_nccl.devs == devs && !g_nccl.comms.empty()) return QB_OK;
+  for (ncclComm_t c : g_nccl.comms) g_nccl.comm_destroy(c);
+  g_nccl.comms.assign(devs.size(), nullptr);
+  g_nccl.devs.clear();
+  const ncclResult_t r = g_nccl.comm_init_all(g_nccl.comms.data(), (int)devs.size(), devs.data());
+  if (r != ncclSuccess) {
+    g_nccl.comms.clear();
+    return fail(QB_E_CUDA, std::string("ncclCommInitAll: ") + g_nccl.error_string(r));
+  }
+  g_nccl.devs = devs;
+  return QB_OK;
 }
 
 // ------------------------------------------------------------------ planning
@@ -673,15 +744,24 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   std::memset(out, 0, sizeof(*out));
   cudaKernel_t imm_fn = nullptr;
+  if (imm && variant == QB_VARIANT_AUTO) {
+    const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 3.0e13 * 1e3;
+    imm = imm_auto(dev, L, imm_hash(L, P.Tc2), est_ms);
+  }
+  double module_ms = 0.0;
   if (imm) {
     bool loaded = false;
-    if (int rc = imm_kernel(dev, L, P.Tc2, &imm_fn, &loaded)) {
+    const auto tm0 = std::chrono::steady_clock::now();
+    const int rc_imm = imm_kernel(dev, L, P.Tc2, &imm_fn, &loaded);
+    if (loaded) module_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
+    if (int rc = rc_imm) {
       if (variant == QB_VARIANT_IMM) return rc;
       imm = false;  // AUTO: the table-load coarse kernel (same results) -- reported in out->variant
     }
     QB_TMARK("imm_module");
   }
   P.imm_one = 1;
+  out->module_ms = module_ms;
   out->variant = fieldwalk ? QB_VARIANT_FIELDWALK
                  : tc      ? QB_VARIANT_TC
                  : imm     ? QB_VARIANT_IMM
@@ -1202,6 +1282,23 @@ int qb_solve_devices(const double* coeffs, int n, int m_fix, uint64_t suffix, in
   std::vector<qb_result> parts((size_t)ndev);
   std::vector<int> rcs((size_t)ndev, QB_OK);
   std::vector<std::string> errs((size_t)ndev);
+  // NCCL combine: every device distinct (a communicator holds each GPU once), libnccl loadable, and
+  // QB_NCCL not "0"; QB_NCCL=1 also takes it for a single device.  Otherwise the host combine below.
+  std::vector<int> devs(devices, devices + ndev);
+  std::vector<int> sorted_devs = devs;
+  std::sort(sorted_devs.begin(), sorted_devs.end());
+  const bool distinct = std::adjacent_find(sorted_devs.begin(), sorted_devs.end()) == sorted_devs.end();
+  const char* env = std::getenv("QB_NCCL");
+  const bool want_nccl = !(env && env[0] == '0') && distinct && (ndev > 1 || (env && env[0] == '1'));
+  std::unique_lock<std::mutex> nccl_lock(qb::g_nccl.mu, std::defer_lock);
+  bool use_nccl = false;
+  if (want_nccl && qb::nccl_load()) {
+    nccl_lock.lock();
+    if (int rc = qb::nccl_comms(devs)) return rc;
+    use_nccl = true;
+  }
+  const size_t nslots = 3 * (size_t)ndev;
+  std::vector<std::vector<long long>> gathered((size_t)ndev);
   std::vector<std::thread> pool;
   for (int i = 0; i < ndev; ++i)
     pool.emplace_back([&, i] {
@@ -1209,17 +1306,67 @@ int qb_solve_devices(const double* coeffs, int n, int m_fix, uint64_t suffix, in
       if (rcs[i] == QB_OK)
         rcs[i] = qb::solve_impl(coeffs, n, m_fix, suffix, m_tie, tie_rule, (uint32_t)i, (uint32_t)ndev, variant,
                                 &parts[i]);
-      if (rcs[i] != QB_OK) errs[i] = qb_last_error();
+      if (rcs[i] == QB_OK && use_nccl) {
+        // one all-reduce(MIN) per rank on its own communicator: the all-gather of the shard keys
+        auto& g = gathered[i];
+        g.assign(nslots, LLONG_MAX);
+        g[i] = (long long)(parts[i].value_key ^ (1ull << 63));  // order-preserving uint64 -> int64
+        g[ndev + i] = (long long)(parts[i].tie_key ^ (1ull << 63));
+        g[2 * ndev + i] = (long long)parts[i].argmin_bits;
+        long long* d = nullptr;
+        cudaStream_t st = nullptr;
+        cudaError_t e = cudaMalloc(&d, nslots * sizeof(long long));
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d, g.data(), nslots * sizeof(long long), cudaMemcpyHostToDevice, st);
+        ncclResult_t nr = ncclSuccess;
+        if (e == cudaSuccess) nr = qb::g_nccl.all_reduce(d, d, nslots, ncclInt64, ncclMin, qb::g_nccl.comms[i], st);
+        if (e == cudaSuccess && nr == ncclSuccess)
+          e = cudaMemcpyAsync(g.data(), d, nslots * sizeof(long long), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && nr == ncclSuccess) e = cudaStreamSynchronize(st);
+        if (st) cudaStreamDestroy(st);
+        if (d) cudaFree(d);
+        if (e != cudaSuccess || nr != ncclSuccess) {
+          rcs[i] = QB_E_CUDA;
+          errs[i] = e != cudaSuccess ? std::string("combine: ") + cudaGetErrorString(e)
+                                     : std::string("ncclAllReduce: ") + qb::g_nccl.error_string(nr);
+          return;
+        }
+      }
+      if (rcs[i] != QB_OK && errs[i].empty()) errs[i] = qb_last_error();
     });
   for (auto& t : pool) t.join();
   for (int i = 0; i < ndev; ++i)
     if (rcs[i] != QB_OK) return qb::fail(rcs[i], "shard " + std::to_string(i) + ": " + errs[i]);
+  if (use_nccl) {
+    // every rank holds the same gathered keys; the winner is picked from rank 0's copy and must be the
+    // shard the host rule below picks (a disagreement would be a transport error)
+    for (int i = 1; i < ndev; ++i)
+      if (gathered[i] != gathered[0]) return qb::fail(QB_E_INTERNAL, "NCCL combine: ranks disagree");
+    const auto& g = gathered[0];
+    for (int i = 0; i < ndev; ++i)
+      if (((unsigned long long)g[i] ^ (1ull << 63)) != parts[i].value_key)
+        return qb::fail(QB_E_INTERNAL, "NCCL combine: gathered key mismatch");
+  }
+  // winner: lexicographic minimum of (value key, tie key) -- from the NCCL-gathered keys when the
+  // device combine ran, else from the host copies of the shard results
   int w = -1;
   for (int i = 0; i < ndev; ++i) {
     if (parts[i].states == 0) continue;
-    if (w < 0 || parts[i].value_key < parts[w].value_key ||
-        (parts[i].value_key == parts[w].value_key && parts[i].tie_key < parts[w].tie_key))
+    unsigned long long vk = parts[i].value_key, tk = parts[i].tie_key;
+    if (use_nccl) {
+      vk = (unsigned long long)gathered[0][i] ^ (1ull << 63);
+      tk = (unsigned long long)gathered[0][ndev + i] ^ (1ull << 63);
+    }
+    if (w < 0) {
       w = i;
+      continue;
+    }
+    unsigned long long wvk = parts[w].value_key, wtk = parts[w].tie_key;
+    if (use_nccl) {
+      wvk = (unsigned long long)gathered[0][w] ^ (1ull << 63);
+      wtk = (unsigned long long)gathered[0][ndev + w] ^ (1ull << 63);
+    }
+    if (vk < wvk || (vk == wvk && tk < wtk)) w = i;
   }
   if (w < 0 || parts[w].value_key == ~0ull) return qb::fail(QB_E_INTERNAL, "no shard produced a result");
   qb_result r = parts[w];
@@ -1239,6 +1386,7 @@ int qb_solve_devices(const double* coeffs, int n, int m_fix, uint64_t suffix, in
     r.collect_ms = std::max(r.collect_ms, parts[i].collect_ms);
     r.exact &= parts[i].exact;
   }
+  r.combine = use_nccl ? 1 : 0;
   r.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   *out = r;
   return QB_OK;
@@ -1299,6 +1447,42 @@ int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, con
 int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                    double* kernel_ms) {
   return qb::batch_impl(coeffs, n, count, argmin_bits, values, kernel_ms);
+}
+
+int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const int* devices, int ndev,
+                           uint64_t* argmin_bits, double* values, double* kernel_ms) {
+  if (!coeffs || !devices || !argmin_bits || !values) return qb::fail(QB_E_ARG, "null pointer");
+  if (ndev < 1 || ndev > 64) return qb::fail(QB_E_ARG, "ndev must be in [1, 64]");
+  if (n < 1) return qb::fail(QB_E_ARG, "dimension must be at least 1");
+  int c = 0;
+  qb_device_count(&c);
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= c) return qb::fail(QB_E_ARG, "device index out of range");
+  // contiguous slices of the instances, slice i on devices[i] from its own host thread; a device listed
+  // twice runs its slices one after another (per-device mutex)
+  std::vector<int> rcs((size_t)ndev, QB_OK);
+  std::vector<std::string> errs((size_t)ndev);
+  std::vector<double> ms((size_t)ndev, 0.0);
+  std::vector<std::thread> pool;
+  const size_t per_inst = (size_t)n * n;
+  for (int i = 0; i < ndev; ++i)
+    pool.emplace_back([&, i] {
+      const uint64_t b0 = count * (uint64_t)i / (uint64_t)ndev, b1 = count * (uint64_t)(i + 1) / (uint64_t)ndev;
+      if (b0 == b1) return;
+      rcs[i] = qb_init(devices[i]);
+      if (rcs[i] == QB_OK)
+        rcs[i] = qb::batch_impl(coeffs + b0 * per_inst, n, b1 - b0, argmin_bits + b0, values + b0, &ms[i]);
+      if (rcs[i] != QB_OK) errs[i] = qb_last_error();
+    });
+  for (auto& t : pool) t.join();
+  for (int i = 0; i < ndev; ++i)
+    if (rcs[i] != QB_OK) {
+      // instance indices in a slice's message are slice-relative: report the slice offset too
+      const uint64_t b0 = count * (uint64_t)i / (uint64_t)ndev;
+      return qb::fail(rcs[i], "slice " + std::to_string(i) + " (instances from " + std::to_string(b0) + "): " + errs[i]);
+    }
+  if (kernel_ms) *kernel_ms = *std::max_element(ms.begin(), ms.end());
+  return QB_OK;
 }
 
 int qb_imm_image(int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size) {

@@ -35,6 +35,9 @@ constexpr int CB = QB_PACKED_ROWS ? (1 << 13) : (1 << 14);  // field bias of Bw 
 #ifndef QB_LDC_MASK
 #define QB_LDC_MASK 0x4040  // table rows u (bit u) taking the per-lane LDC + VIADDMNMX path (measured)
 #endif
+#ifndef QB_IMM_FUSED
+#define QB_IMM_FUSED 14  // patched-immediate pass: of the 30 pairs after the first two per row, those folded by the fused VIADDMNMX (ALU pipe); measured 10: 31.6, 12: 30.1, 14: 29.7, 16: 30.3 ms (n=40)
+#endif
 #ifndef QB_EXACT_NOINLINE
 #define QB_EXACT_NOINLINE 0  // 1: long chunks call the exact re-evaluation out of line (won 52 -> 41 ms before the host seed; inline measured 33.99 -> 33.70 ms since)
 #endif
@@ -71,8 +74,9 @@ __device__ __forceinline__ unsigned add_fma_pipe(unsigned a, unsigned one, unsig
 
 // Coarse minimum over the 2^B states of a block, in coarse units (exact integer arithmetic).
 // IMM: the table words are instruction immediates (patched per instance) instead of constant-bank
-// loads; per row of 32 pairs, 22 pairs are formed by IMAD (FMA pipe) and folded by VIMNMX3, 10 by
-// the fused VIADDMNMX (ALU pipe): ~0.71 issue slots per state, both pipes ~equally loaded.
+// loads.  Integer adds run on the FMA-heavy pipe (IMAD) or the ALU pipe, each one warp-instruction
+// per 2 cycles per SMSP, so the pass balances the two: per row of 32 pairs, QB_IMM_FUSED pairs fold
+// through the fused VIADDMNMX (ALU) and the rest are IMAD adds (FMA-heavy) folded by VIMNMX3 (ALU).
 template <int B1, int B2, bool IMM = false>
 __device__ __forceinline__ int coarse_block_min(const TableParams& p, const float (&H)[B1 + B2]) {
   constexpr int B = B1 + B2, NU = 1 << B1, NP = 1 << (B2 - 1);
@@ -103,29 +107,52 @@ __device__ __forceinline__ int coarse_block_min(const TableParams& p, const floa
   unsigned rmin2 = 0u;
   if constexpr (IMM) {
     const unsigned one = p.imm_one;
+    // rows in reflected Gray order of u: each row's A2 is the previous one +- one packed field, so the
+    // 16 A2 values are never live at once (16 registers fewer than the table-load path)
+    unsigned du[B1];
 #pragma unroll
-    for (int u = 0; u < NU; u += 2) {
+    for (int i = 0; i < B1; ++i) du[i] = (unsigned)hc[B2 + i] * 0x10001u;
+    unsigned a2 = (unsigned)(2 * CB) * 0x10001u;
+#pragma unroll
+    for (int g = 0; g < NU; g += 2) {
       unsigned r2[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const unsigned ph = QB_IMM_PH | (unsigned)((u + h) * NP);
-        unsigned acc = 0u, f0 = 0xffffffffu, f1 = 0xffffffffu;
+        const int gg = g + h, u = gg ^ (gg >> 1);
+        if (gg) {
+          const int i = (gg & 1) ? 0 : (gg & 2) ? 1 : (gg & 4) ? 2 : 3;  // ctz(gg), gg < 16
+          a2 = ((u >> i) & 1) ? a2 + du[i] : a2 - du[i];
+        }
+        const unsigned ph = QB_IMM_PH | (unsigned)(u * NP);
+        // the first two pairs (FMA-pipe adds) start two accumulators; of the remaining NP - 2 pairs,
+        // QB_IMM_FUSED (spread evenly) fold through VIADDMNMX and the rest are FMA-pipe adds folded two
+        // at a time by VIMNMX3, alternating between the accumulators
+        unsigned acc[2] = {add_fma_pipe(Bw2[0], one, ph | 0u), add_fma_pipe(Bw2[1], one, ph | 1u)};
+        unsigned pend = 0u;
+        int npend = 0, nfold = 0;
 #pragma unroll
-        for (int m = 0; m < NP; m += 3) {
-          if (m + 1 < NP) {
-            const unsigned c0 = add_fma_pipe(Bw2[m], one, ph | m), c1 = add_fma_pipe(Bw2[m + 1], one, ph | (m + 1));
-            acc = (m == 0) ? umin2(c0, c1) : umin3(acc, c0, c1);
-          }
-          if (m + 2 < NP) {
-            if ((m / 3) & 1)
-              f1 = __viaddmin_u16x2(Bw2[m + 2], ph | (m + 2), f1);
-            else
-              f0 = __viaddmin_u16x2(Bw2[m + 2], ph | (m + 2), f0);
+        for (int m = 2; m < NP; ++m) {
+          const int q = m - 2;
+          const bool fused = ((q + 1) * QB_IMM_FUSED) / (NP - 2) > (q * QB_IMM_FUSED) / (NP - 2);
+          if (fused) {
+            acc[nfold & 1] = __viaddmin_u16x2(Bw2[m], ph | m, acc[nfold & 1]);
+            ++nfold;
+          } else {
+            const unsigned c = add_fma_pipe(Bw2[m], one, ph | m);
+            if (npend == 0) {
+              pend = c;
+              npend = 1;
+            } else {
+              acc[nfold & 1] = umin3(acc[nfold & 1], pend, c);
+              ++nfold;
+              npend = 0;
+            }
           }
         }
-        r2[h] = umin3(acc, f0, f1) + A2[u + h];
+        if (npend) acc[0] = umin2(acc[0], pend);
+        r2[h] = umin2(acc[0], acc[1]) + a2;
       }
-      rmin2 = (u == 0) ? umin2(r2[0], r2[1]) : umin3(rmin2, r2[0], r2[1]);
+      rmin2 = (g == 0) ? umin2(r2[0], r2[1]) : umin3(rmin2, r2[0], r2[1]);
     }
     return (int)min(rmin2 & 0xffffu, rmin2 >> 16) - 4 * CB;
   } else {

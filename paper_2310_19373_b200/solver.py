@@ -219,19 +219,23 @@ def _batch_coeffs(instances) -> np.ndarray:
     return np.ascontiguousarray(np.stack([i.coeffs for i in insts]))
 
 
-def solve_batch(instances, *, as_arrays: bool = False):
+def solve_batch(instances, *, as_arrays: bool = False, devices=None):
     """Solve many independent instances of one size n <= 24 in one GPU launch (one CTA per
     instance).  Each result equals ``solve_incremental`` of that instance (same tie rule).
     ``instances``: a sequence of QuboInstance or a (count, n, n) array.  Returns a list of
     Solution, or with ``as_arrays=True`` the pair (minimizers uint8 (count, n), values (count,)).
     The reference has no batch entry point; its equivalent is a loop / thread pool of
-    solve_incremental calls."""
+    solve_incremental calls.  ``devices``: CUDA devices of this process to
+    split the instances over (contiguous slices, qb_solve_batch_devices); None = the current device."""
     coeffs = _batch_coeffs(instances)
     count, n = coeffs.shape[0], coeffs.shape[1]
     if count == 0:
         return (np.zeros((0, n), dtype=np.uint8), np.zeros(0)) if as_arrays else []
     t0 = time.perf_counter()
-    bits, vals, _ = _lib.solve_batch(coeffs)
+    if devices is None:
+        bits, vals, _ = _lib.solve_batch(coeffs)
+    else:
+        bits, vals, _ = _lib.solve_batch_devices(coeffs, SolveConfig(devices=devices).devices)
     # bit i of each little-endian uint64 -> column i (one vectorised pass, no per-bit shifts)
     minimizers = np.unpackbits(bits.astype("<u8").view(np.uint8).reshape(count, 8), axis=1,
                                bitorder="little")[:, :n]

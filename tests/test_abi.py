@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_result_struct_layout():
-    assert ctypes.sizeof(_lib.QbResult) == 112
+    assert ctypes.sizeof(_lib.QbResult) == 128
     assert _lib.QbResult.kernel_ms.offset == 64
 
 

@@ -29,8 +29,10 @@ def test_imm_equals_table_load_coarse(name, n, rep):
     got = _lib.solve(c, variant=_lib.VARIANT_IMM)
     assert got.variant == _lib.VARIANT_IMM and ref.variant == _lib.VARIANT_COARSE
     assert _same(got, ref), (name, n, rep)
-    auto = _lib.solve(c)
-    assert auto.variant == _lib.VARIANT_IMM and _same(auto, ref)
+    auto = _lib.solve(c)  # AUTO: this table was solved (and loaded) just above -> the patched kernel
+    assert _same(auto, ref)
+    if ref.variant == _lib.VARIANT_COARSE and auto.variant != _lib.VARIANT_TABLE:
+        assert auto.variant == _lib.VARIANT_IMM
 
 
 @pytest.mark.parametrize("m_fix,m_tie,shards", [(0, 6, 1), (0, 0, 3), (4, 4, 1), (2, 9, 2)])
@@ -63,6 +65,18 @@ def test_imm_vs_oracle_subspace_n34():
     assert got.variant == _lib.VARIANT_IMM
     bits, val, _ = O.solve_subspaces(c, m, suffix, suffix + 1, threads=8)
     assert int(got.argmin_bits) == bits and got.value == val
+
+
+def test_auto_policy_first_solve_and_repeat():
+    """AUTO takes the patched kernel on a first solve only when the search is long (n=40), and on
+    the repeat of a table it has seen (n=33); a first n=33 solve stays on the table-load kernel."""
+    c33 = instances.config_coeffs("E", 41, n=33)
+    first = _lib.solve(c33)
+    again = _lib.solve(c33)
+    assert first.variant == _lib.VARIANT_COARSE and again.variant == _lib.VARIANT_IMM
+    assert _same(first, again)
+    c40 = instances.config_coeffs("E", 42, n=40)
+    assert _lib.solve(c40).variant == _lib.VARIANT_IMM
 
 
 def test_imm_adversarial_ranges():

@@ -575,3 +575,17 @@ def test_bench_records_match_reference_bench(bench_golden):
     text = io.StringIO()
     benchrec.write_csv(recs, stream=text)
     assert benchrec.parse_csv(text.getvalue()) == recs
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0], [0]])
+def test_batch_across_devices_gathers_in_order(golden, devices):
+    """Config C split over a device list (one slice per entry): the gathered answers
+    equal the reference's 4096 golden results in order; odd counts and more slices than instances."""
+    cb = golden["configC"]
+    batch = instances.config_batch(cb["count"], cb["n"])
+    bits, vals, _ = _lib.solve_batch_devices(batch, devices)
+    assert [int(b) for b in bits] == cb["bits"]
+    assert vals.tolist() == cb["values"]
+    mins, mvals = qb.solve_batch(batch[:5], as_arrays=True, devices=devices + [0, 0, 0, 0])
+    assert [qb.bits_to_int(m) for m in mins] == cb["bits"][:5]
+    assert mvals.tolist() == cb["values"][:5]

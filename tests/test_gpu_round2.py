@@ -144,3 +144,19 @@ def test_collect_lists_regrow_on_overflow():
     assert r.value == O.eval_upper(inst.coeffs, qb.bits_from_int(want, n).astype(np.float64))
     sol = qb.solve_incremental(inst)
     assert _bits(sol) == want
+
+
+# ------------------------------------------------------------------ single-process NCCL combine
+def test_solve_devices_nccl_combine(monkeypatch):
+    """qb_solve_devices combines shards with one ncclAllReduce(MIN) when its devices are distinct
+    (QB_NCCL=1 takes that path for the single GPU here, a one-rank communicator); the answer equals
+    the one-launch solve.  With a repeated device the host combine runs (combine == 0)."""
+    c = instances.config_coeffs("D", 5, n=30)
+    whole = _lib.solve(c)
+    monkeypatch.setenv("QB_NCCL", "1")
+    r = _lib.solve_devices(c, [0])
+    assert r.combine == 1
+    assert (r.argmin_bits, r.value, r.tie_key) == (whole.argmin_bits, whole.value, whole.tie_key)
+    r2 = _lib.solve_devices(c, [0, 0])
+    assert r2.combine == 0
+    assert (r2.argmin_bits, r2.value, r2.tie_key) == (whole.argmin_bits, whole.value, whole.tie_key)

@@ -66,14 +66,17 @@ for op, nexec in by.most_common(14):
     print(f"  {op:10s} {nexec * 32 / states:.3f}/state")
 
 if record:
-    from bench import kernel_symbol, sass_sha256
+    from bench import imm_sass_sha256, imm_symbol, kernel_symbol, sass_sha256
 
     name = out["Kernel Name"][0]
-    m = re.search(r"(\w+)<([\d, ]+)>", name)
-    fam, targs = m.group(1), [int(t) for t in m.group(2).split(",")]
+    m = re.search(r"(\w+)<([\w, ]+)>", name)
+    fam, targs = m.group(1), [t.strip() for t in m.group(2).split(",")]
     lib_path = os.path.join(ROOT, "paper_2310_19373_b200", "libqubrute_b200.so")
-    sym = kernel_symbol(lib_path, fam, targs[4])
-    sha = sass_sha256(lib_path, sym)
+    if fam == "coarse_kernel" and targs[-1] == "true":  # patched-immediate kernel (embedded cubin)
+        sym, sha = imm_symbol(int(targs[4])), imm_sass_sha256(int(targs[4]))
+    else:
+        sym = kernel_symbol(lib_path, fam, int(targs[4]))
+        sha = sass_sha256(lib_path, sym)
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     dram = sum(float(out[k][0]) * scale[out[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     path = os.path.join(ROOT, "profiles", "kernel_records.json")
