@@ -464,8 +464,8 @@ def main():
             distributed.allreduce_argmin(res)
         return res
 
-    for _ in range(args.warmup):
-        device_step()
+    warm = [device_step() for _ in range(args.warmup)]
+    module_ms = max(float(w.module_ms) for w in warm) if warm else 0.0
     barrier()
 
     # ---- device-time measurement (value)
@@ -524,16 +524,23 @@ def main():
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": int(r.param_bytes) * int(r.launches),
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max * 1e3 / args.steps},
         "gpu_launches": launches,
+        "imm_module": {"load_ms": module_ms,
+                       "note": "the patched-immediate search kernel (QB_VARIANT_IMM) is built for an instance by "
+                               "writing its coarse table into a cubin copy and loading it (first solve of a table, "
+                               "in the warm-up here); later solves of the same table reuse the loaded module, as "
+                               "the timed value and e2e steps do"},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_extra:
         line["configs"] = extra_configs(qb, _lib, instances)
-        # the other traversal kernels on the same workload: the fp32 table kernel, the literal
-        # per-step field walk and the tensor-core coarse pass (QB_VARIANT_TABLE / _FIELDWALK / _TC)
-        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse", 4: "tc"}
+        # the other traversal kernels on the same workload: the table-load coarse kernel, the fp32 table
+        # kernel and the literal per-step field walk (QB_VARIANT_COARSE / _TABLE / _FIELDWALK)
+        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse_tableload", 4: "tc", 5: "coarse_imm"}
         line["variants"] = {f"{names[int(r.variant)]} (default)": {
             "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
-        for var in (_lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK, _lib.VARIANT_TC):
+        # (the tensor-core pass, QB_VARIANT_TC, is retired from this list: 40 ms, TMEM round-trip bound,
+        # DESIGN.md section 4)
+        for var in (_lib.VARIANT_COARSE, _lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK):
             _lib.solve(inst.coeffs, variant=var)
             vr = _lib.solve(inst.coeffs, variant=var)
             vs = states / (vr.search_ms * 1e-3)

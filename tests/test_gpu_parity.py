@@ -177,9 +177,11 @@ def test_config_e_n40_properties():
     inst = qb.QuboInstance(c)
     sol = qb.solve_incremental(inst)
     auto = _lib.solve(c)
-    assert auto.variant == _lib.VARIANT_COARSE
+    assert auto.variant == _lib.VARIANT_IMM  # n=40: the patched-immediate coarse kernel
     table = _lib.solve(c, variant=_lib.VARIANT_TABLE)
-    assert (auto.argmin_bits, auto.value, auto.tie_key) == (table.argmin_bits, table.value, table.tie_key)
+    coarse = _lib.solve(c, variant=_lib.VARIANT_COARSE)
+    for other in (table, coarse):
+        assert (auto.argmin_bits, auto.value, auto.tie_key) == (other.argmin_bits, other.value, other.tie_key)
     x = _bits(sol)
     assert sol.value == O.eval_upper(c, sol.minimizer.astype(np.float64))
     m = 17  # 2^23-state subspaces
@@ -555,8 +557,10 @@ def test_n40_other_instance_types(name):
     c = instances.config_coeffs(name, 0, n=40)
     a = _lib.solve(c)
     b = _lib.solve(c, variant=_lib.VARIANT_TABLE)
-    assert a.variant == _lib.VARIANT_COARSE and b.variant == _lib.VARIANT_TABLE
+    d = _lib.solve(c, variant=_lib.VARIANT_COARSE)
+    assert a.variant == _lib.VARIANT_IMM and b.variant == _lib.VARIANT_TABLE and d.variant == _lib.VARIANT_COARSE
     assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key)
+    assert (a.argmin_bits, a.value, a.tie_key) == (d.argmin_bits, d.value, d.tie_key)
     x = int(a.argmin_bits)
     m = 17
     bits, val, _ = O.solve_subspaces(c, m, x >> (40 - m), (x >> (40 - m)) + 1)

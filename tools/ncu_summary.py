@@ -72,7 +72,7 @@ if record:
     m = re.search(r"(\w+)<([\w, ]+)>", name)
     fam, targs = m.group(1), [t.strip() for t in m.group(2).split(",")]
     lib_path = os.path.join(ROOT, "paper_2310_19373_b200", "libqubrute_b200.so")
-    if fam == "coarse_kernel" and targs[-1] == "true":  # patched-immediate kernel (embedded cubin)
+    if fam == "coarse_kernel" and len(targs) > 6 and targs[6] in ("true", "1"):  # patched-immediate kernel (embedded cubin)
         sym, sha = imm_symbol(int(targs[4])), imm_sass_sha256(int(targs[4]))
     else:
         sym = kernel_symbol(lib_path, fam, int(targs[4]))
