@@ -85,9 +85,10 @@ def sass_sha256(lib_path: str, symbol: str):
     return hashlib.sha256("\n".join(body).encode()).hexdigest()
 
 
-def imm_sass_sha256(L: int):
-    """sha256 of the SASS of the patched-immediate coarse kernel for chunk length L with its
-    placeholders in place (the code, independent of any instance's table words), or None."""
+def imm_sass_sha256(L: int, kind: int = 1):
+    """sha256 of the SASS of a patched-immediate coarse kernel (kind 1: 10-bit, 2: super-block) for
+    chunk length L with its placeholders in place (the code, independent of any instance's table
+    words), or None."""
     import tempfile
 
     import numpy as np
@@ -95,16 +96,18 @@ def imm_sass_sha256(L: int):
     from paper_2310_19373_b200 import _lib
 
     try:
-        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(512, dtype=np.uint32))
+        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(512 * kind, dtype=np.uint32), kind)
     except Exception:  # noqa: BLE001 - no cubin for this L / library without the IMM kernels
         return None
     with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
         fh.write(img)
         fh.flush()
-        return sass_sha256(fh.name, imm_symbol(L))
+        return sass_sha256(fh.name, imm_symbol(L, kind))
 
 
-def imm_symbol(L: int) -> str:
+def imm_symbol(L: int, kind: int = 1) -> str:
+    if kind == 2:
+        return f"_ZN2qb14coarse2_kernelILi5ELi5ELi{L}ELi128EEEvNS_11TableParamsE"
     return f"_ZN2qb13coarse_kernelILi5ELi5ELi4ELi6ELi{L}ELi128ELb1EEEvNS_11TableParamsE"
 
 
@@ -141,7 +144,8 @@ def fp32_lane_peak_per_sm_clk():
         return FP32_ADD_LANES_PER_SM_CLK, "fallback 128 FP32 lanes/SM/clk"
 
 
-FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel", 5: "coarse_kernel (imm)"}
+FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel", 5: "coarse_kernel (imm)",
+            6: "coarse2_kernel (imm)"}
 
 
 def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path):
@@ -154,8 +158,9 @@ def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path)
     state's value with ~1 instruction instead of n+1 additions."""
     L = n - int(r.prefix_bits)
     family = FAMILIES.get(int(r.variant))
-    if int(r.variant) == 5:  # patched-immediate kernel: SASS of the embedded cubin, placeholders in place
-        sym, sha = imm_symbol(L), imm_sass_sha256(L)
+    if int(r.variant) in (5, 6):  # patched-immediate kernels: SASS of the embedded cubin, placeholders in place
+        kind = int(r.variant) - 4
+        sym, sha = imm_symbol(L, kind), imm_sass_sha256(L, kind)
     else:
         sym = kernel_symbol(lib_path, family, L) if family else None
         sha = sass_sha256(lib_path, sym) if sym else None
@@ -535,12 +540,13 @@ def main():
         line["configs"] = extra_configs(qb, _lib, instances)
         # the other traversal kernels on the same workload: the table-load coarse kernel, the fp32 table
         # kernel and the literal per-step field walk (QB_VARIANT_COARSE / _TABLE / _FIELDWALK)
-        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse_tableload", 4: "tc", 5: "coarse_imm"}
+        names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse_tableload", 4: "tc", 5: "coarse_imm",
+                 6: "coarse_imm_superblock"}
         line["variants"] = {f"{names[int(r.variant)]} (default)": {
             "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
         # (the tensor-core pass, QB_VARIANT_TC, is retired from this list: 40 ms, TMEM round-trip bound,
         # DESIGN.md section 4)
-        for var in (_lib.VARIANT_COARSE, _lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK):
+        for var in (_lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK):
             _lib.solve(inst.coeffs, variant=var)
             vr = _lib.solve(inst.coeffs, variant=var)
             vs = states / (vr.search_ms * 1e-3)

@@ -48,7 +48,9 @@ extern "C" {
 #define QB_VARIANT_COARSE 3    /* table walk with a packed-int16 block pass + exact re-evaluation */
 #define QB_VARIANT_TC 4        /* coarse block pass formed by tcgen05.mma (f16, TMEM) + exact re-evaluation */
 #define QB_VARIANT_IMM 5       /* coarse kernel with the instance's coarse table patched into its SASS as
-                                  instruction immediates (no table loads); AUTO's choice where COARSE runs */
+                                  instruction immediates (no table loads), 10-bit blocks */
+#define QB_VARIANT_IMM2 6      /* the same with 11-bit coarse super-blocks (two blocks per coarse pass, chunks
+                                  of >= 12 free bits); AUTO's choice where COARSE runs */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {
@@ -149,10 +151,11 @@ int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const in
 int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_t count, double* values,
                    double* fields);
 
-/* Test hook (host only): the embedded patched-immediate cubin for chunk length L with the 512 coarse
- * table words `words` written into its placeholder immediates -- the image QB_VARIANT_IMM loads.
+/* Test hook (host only): the embedded patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 512 coarse
+ * table words; 2: QB_VARIANT_IMM2, 1024 words) for chunk length L with `words` written into its
+ * placeholder immediates -- the image those variants load.
  * *size receives the image size; the image is copied to `out` when cap >= *size. */
-int qb_imm_image(int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);
+int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,9 @@ SOURCES = [os.path.join(PKG_DIR, "csrc", f)
 DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]
 # patched-immediate coarse kernels (QB_VARIANT_IMM): one cubin per chunk length, embedded in the .so
 IMM_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse_imm.cu")
+IMM2_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse2_imm.cu")
 IMM_LS = (10, 11, 12, 13, 14, 16, 18, 20, 22)
+IMM2_LS = (12, 13, 14, 16, 18, 20, 22)  # super-block kernel: chunks of >= B + 2 free bits
 
 QB_OK = 0
 QB_E_ARG = -1
@@ -42,6 +44,7 @@ VARIANT_FIELDWALK = 2
 VARIANT_COARSE = 3
 VARIANT_TC = 4
 VARIANT_IMM = 5
+VARIANT_IMM2 = 6
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -107,8 +110,8 @@ SIGNATURES = {
     "qb_solve_batch_devices": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int),
                                               ctypes.c_int, _u64p, _dp, _dp]),
     "qb_prefix_eval": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _dp, _dp]),
-    "qb_imm_image": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.c_char_p, ctypes.c_uint64,
-                                    _u64p]),
+    "qb_imm_image": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.c_char_p,
+                                    ctypes.c_uint64, _u64p]),
 }
 
 _lock = threading.Lock()
@@ -141,12 +144,13 @@ def build(force: bool = False, verbose: bool = False, output: str | None = None,
         procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
     cubins = []
-    for L in IMM_LS:
-        cub = os.path.join(objdir, f"qb_coarse_imm_L{L}.cubin")
-        cmd = ["nvcc", *[f for f in compile_flags if not f.startswith("-Xcompiler") and "-fPIC" not in f],
-               f"-DQB_IMM_L={L}", "-cubin", "-o", cub, IMM_SOURCE]
-        procs.append((f"{IMM_SOURCE} (L={L})", subprocess.Popen(cmd)))
-        cubins.append((L, cub))
+    for kind, src, Ls in ((1, IMM_SOURCE, IMM_LS), (2, IMM2_SOURCE, IMM2_LS)):
+        for L in Ls:
+            cub = os.path.join(objdir, f"qb_coarse_imm{kind}_L{L}.cubin")
+            cmd = ["nvcc", *[f for f in compile_flags if not f.startswith("-Xcompiler") and "-fPIC" not in f],
+                   f"-DQB_IMM_L={L}", "-cubin", "-o", cub, src]
+            procs.append((f"{src} (L={L})", subprocess.Popen(cmd)))
+            cubins.append((kind, L, cub))
     failed = [src for src, p in procs if p.wait() != 0]
     if failed:
         raise subprocess.CalledProcessError(1, f"nvcc {failed}")
@@ -163,17 +167,17 @@ def _embed_cubins(objdir: str, cubins) -> str:
     with open(csrc, "w") as fh:
         fh.write("/* generated by paper_2310_19373_b200/_lib.py: patched-immediate coarse cubins */\n")
         fh.write("#include <stddef.h>\n")
-        for L, path in cubins:
+        for kind, L, path in cubins:
             data = open(path, "rb").read()
-            fh.write(f"static const unsigned char cubin_L{L}[{len(data)}] __attribute__((aligned(16))) = {{\n")
+            fh.write(f"static const unsigned char cubin_{kind}_L{L}[{len(data)}] __attribute__((aligned(16))) = {{\n")
             for i in range(0, len(data), 32):
                 fh.write(",".join(str(b) for b in data[i:i + 32]) + ",\n")
             fh.write("};\n")
-        fh.write("struct qb_imm_cubin { int L; const unsigned char* data; size_t size; };\n")
+        fh.write("struct qb_imm_cubin { int kind; int L; const unsigned char* data; size_t size; };\n")
         fh.write("const struct qb_imm_cubin qb_imm_cubins[] = {\n")
-        for L, path in cubins:
-            fh.write(f"  {{{L}, cubin_L{L}, sizeof(cubin_L{L})}},\n")
-        fh.write("  {0, 0, 0}};\n")
+        for kind, L, path in cubins:
+            fh.write(f"  {{{kind}, {L}, cubin_{kind}_L{L}, sizeof(cubin_{kind}_L{L})}},\n")
+        fh.write("  {0, 0, 0, 0}};\n")
     obj = csrc.replace(".c", ".o")
     subprocess.run(["cc", "-O1", "-fPIC", "-c", "-o", obj, csrc], check=True)
     return obj
@@ -335,14 +339,15 @@ def prefix_eval(coeffs, k: int, c_begin: int, count: int, device: int | None = N
     return vals, fields
 
 
-def imm_image(L: int, words) -> bytes:
-    """The patched-immediate cubin for chunk length L with coarse table words `words` (test hook)."""
+def imm_image(L: int, words, kind: int = 1) -> bytes:
+    """The patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 512 words; 2: QB_VARIANT_IMM2, 1024
+    words) for chunk length L with coarse table words `words` (test hook)."""
     w = np.ascontiguousarray(words, dtype=np.uint32)
-    if w.shape != (512,):
-        raise ValueError("need 512 table words")
+    if w.shape != ((512,) if kind == 1 else (1024,)):
+        raise ValueError("need 512 (kind 1) or 1024 (kind 2) table words")
     size = ctypes.c_uint64()
     wp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
-    check(lib().qb_imm_image(L, wp, None, 0, ctypes.byref(size)), "qb_imm_image")
+    check(lib().qb_imm_image(kind, L, wp, None, 0, ctypes.byref(size)), "qb_imm_image")
     buf = ctypes.create_string_buffer(size.value)
-    check(lib().qb_imm_image(L, wp, buf, size.value, ctypes.byref(size)), "qb_imm_image")
+    check(lib().qb_imm_image(kind, L, wp, buf, size.value, ctypes.byref(size)), "qb_imm_image")
     return buf.raw[: size.value]

@@ -229,6 +229,7 @@ static int ensure_host(T** ptr, size_t* cap, size_t need) {
 }  // namespace qb
 extern "C" {
 struct qb_imm_cubin {
+  int kind;  // 1: coarse_kernel<.., IMM = true> (10-bit pass), 2: coarse2_kernel (11-bit super-blocks)
   int L;
   const unsigned char* data;
   size_t size;
@@ -237,13 +238,14 @@ extern const struct qb_imm_cubin qb_imm_cubins[];  // qb_imm_cubins.c, generated
 }
 namespace qb {
 
-constexpr int kImmWords = 1 << (BMAX - 1);  // Tc2 words = placeholders per kernel
+constexpr int kImmWords = 1 << (BMAX - 1);  // Tc2 words = placeholders of the 10-bit kernel
+constexpr int kImm2Words = 1 << BMAX;       // Tc11 words = placeholders of the super-block kernel
 
 // Write words[idx] into every SASS instruction whose 32-bit immediate (bits 32..63 of the first
 // instruction word) is QB_IMM_PH | idx, in every .text section.  Each placeholder must occur exactly
 // once per kernel and only in an add/min instruction with an immediate operand, else the image is
 // rejected (the caller then runs the table-load coarse kernel).
-static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words) {
+static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words, int nwords) {
   auto rd16 = [&](size_t o) { uint16_t v; std::memcpy(&v, &img[o], 2); return v; };
   auto rd32 = [&](size_t o) { uint32_t v; std::memcpy(&v, &img[o], 4); return v; };
   auto rd64 = [&](size_t o) { uint64_t v; std::memcpy(&v, &img[o], 8); return v; };
@@ -258,10 +260,11 @@ static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words) {
     const uint64_t name = stroff + rd32(sh), off = rd64(sh + 24), size = rd64(sh + 32);
     if (name + 6 >= img.size() || std::memcmp(&img[name], ".text.", 6) != 0) continue;
     if (off + size > img.size() || (off & 15) != 0) return false;
-    std::vector<int> seen(kImmWords, 0);
+    std::vector<int> seen((size_t)nwords, 0);
     for (uint64_t at = off; at + 16 <= off + size; at += 16) {
       const uint32_t imm = rd32(at + 4);
-      if ((imm & 0xFFFF0000u) != QB_IMM_PH || (imm & 0xFFFFu) >= (unsigned)kImmWords) continue;
+      if ((imm & 0xFFFF0000u) != QB_IMM_PH) continue;
+      if ((imm & 0xFFFFu) >= (unsigned)nwords) return false;
       // immediate forms of IMAD / VIADD / IADD3 / VIADDMNMX, or a constant materialised by MOV or by
       // HFMA2 R, -RZ, RZ, imm (exact for half2 words without NaN/Inf lanes, checked below)
       const unsigned op = rd16(at) & 0xFFFu;
@@ -283,7 +286,10 @@ static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words) {
   return kernels == 1;
 }
 
-static std::string imm_kernel_name(int L) {
+static std::string imm_kernel_name(int kind, int L) {
+  if (kind == 2)
+    return "_ZN2qb14coarse2_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
+           std::to_string(L) + "ELi" + std::to_string(TPB) + "EEEvNS_11TableParamsE";
   return "_ZN2qb13coarse_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
          std::to_string(QB_COARSE_B1) + "ELi" + std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" +
          std::to_string(TPB) + "ELb1EEEvNS_11TableParamsE";
@@ -291,9 +297,9 @@ static std::string imm_kernel_name(int L) {
 
 // The patched kernel for chunk length L and table words tc2 on this device (cached).  Returns
 // QB_OK with *out set, or a QB_E_* code (no cubin for L, rejected image, load failure).
-static unsigned long long imm_hash(int L, const unsigned* tc2) {
-  unsigned long long h = 1469598103934665603ull ^ (unsigned long long)L;
-  for (int i = 0; i < kImmWords; ++i) h = (h ^ tc2[i]) * 1099511628211ull;
+static unsigned long long imm_hash(int kind, int L, const unsigned* words, int nwords) {
+  unsigned long long h = 1469598103934665603ull ^ (unsigned long long)L ^ ((unsigned long long)kind << 32);
+  for (int i = 0; i < nwords; ++i) h = (h ^ words[i]) * 1099511628211ull;
   return h;
 }
 
@@ -311,8 +317,9 @@ static bool imm_auto(Device* dev, int L, unsigned long long h, double est_ms) {
   return seen || est_ms >= min_ms;
 }
 
-static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out, bool* loaded) {
-  const unsigned long long h = imm_hash(L, tc2);
+static int imm_kernel(Device* dev, int kind, int L, const unsigned* words, int nwords, cudaKernel_t* out,
+                      bool* loaded) {
+  const unsigned long long h = imm_hash(kind, L, words, nwords);
   *loaded = false;
   for (auto& m : dev->imm)
     if (m.lib && m.L == L && m.hash == h) {
@@ -322,8 +329,9 @@ static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out
     }
   const qb_imm_cubin* cb = nullptr;
   for (const qb_imm_cubin* c = qb_imm_cubins; c->data; ++c)
-    if (c->L == L) cb = c;
-  if (!cb) return fail(QB_E_INTERNAL, "no patched-immediate cubin for L=" + std::to_string(L));
+    if (c->L == L && c->kind == kind) cb = c;
+  if (!cb) return fail(QB_E_INTERNAL, "no patched-immediate cubin for kind " + std::to_string(kind) + ", L=" +
+                                          std::to_string(L));
   ImmModule* slot = &dev->imm[0];
   for (auto& m : dev->imm)
     if (!m.lib || m.last_use < slot->last_use) slot = &m;
@@ -332,9 +340,10 @@ static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out
     slot->lib = nullptr;
   }
   slot->image.assign(cb->data, cb->data + cb->size);
-  if (!imm_patch(slot->image, tc2)) return fail(QB_E_INTERNAL, "patched-immediate cubin rejected (placeholders)");
+  if (!imm_patch(slot->image, words, nwords))
+    return fail(QB_E_INTERNAL, "patched-immediate cubin rejected (placeholders)");
   QB_CUDA(cudaLibraryLoadData(&slot->lib, slot->image.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-  const std::string name = imm_kernel_name(L);
+  const std::string name = imm_kernel_name(kind, L);
   cudaError_t e = cudaLibraryGetKernel(&slot->kern, slot->lib, name.c_str());
   if (e != cudaSuccess) {
     cudaLibraryUnload(slot->lib);
@@ -352,6 +361,14 @@ static int imm_kernel(Device* dev, int L, const unsigned* tc2, cudaKernel_t* out
 static bool imm_enabled() {
   const char* e = std::getenv("QB_IMM");
   return !(e && e[0] == '0');
+}
+
+#ifndef QB_IMM_AUTO_KIND
+#define QB_IMM_AUTO_KIND 1  // AUTO's patched-immediate kernel: 1 = 10-bit blocks (n=40: 29.6 ms), 2 = 11-bit super-blocks (30.3 ms)
+#endif
+static int imm_auto_kind() {
+  const char* e = std::getenv("QB_IMM_KIND");
+  return e ? std::atoi(e) : QB_IMM_AUTO_KIND;
 }
 
 // ------------------------------------------------------------------ NCCL combine (qb_solve_devices)
@@ -409,6 +426,7 @@ struct Plan {
   long long Eq = 0;  // bound on |quantized - exact * 2^e| for any state (quantized units)
   KernelSet* ks = nullptr;
   std::unique_ptr<TableParams> P;
+  std::vector<unsigned> imm2_words;  // 11-bit coarse table (super-block kernel), 1024 packed words
 };
 
 static double sym(const double* c, int n, int i, int j) {
@@ -419,7 +437,8 @@ static double sym(const double* c, int n, int i, int j) {
 // BE: block bits (their relative values are formed in fp32); B: table bits (T is built over them).
 static long long seed_greedy(const std::vector<double>& q, int n);
 
-static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false, bool seed = false) {
+static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false, bool seed = false,
+                    bool imm2_image = false) {
   const double LIM = 16777215.0;  // 2^24 - 1
   auto bound = [&](auto get) {
     double r_in = 0.0, rmax = 0.0;
@@ -517,6 +536,34 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
     const int t0 = (z < (1 << B)) ? (int)std::nearbyint((double)P.T[z] * cscale) : 0;
     const int t1 = (z + 1 < (1 << B)) ? (int)std::nearbyint((double)P.T[z + 1] * cscale) : 0;
     P.Tc2[z / 2] = (unsigned)(t0 + bias) | ((unsigned)(t1 + bias) << 16);
+  }
+  if (imm2_image && B == BMAX && n > B) {
+    // 11-bit coarse image of the super-block kernel (qb_coarse2.cuh): bits 0..B-1 plus bit B.
+    // T11(z | b << B) = T(z) + b (q_BB + sum_{i<B} z_i q_iB); coarse unit 2^s11 with s11 the smallest
+    // shift for which rows 0..B of |q| fit the biased 15-bit fields (the same rule over one more row)
+    double rq11 = 0.0;
+    for (int i = 0; i <= B; ++i)
+      for (int j = i; j < n; ++j) rq11 += std::fabs(q[(size_t)i * n + j]);
+    int cs11 = 0;
+    while (std::ldexp(rq11, -cs11) + (B + 1) + 2 > field_max) ++cs11;
+    const double sc11 = std::ldexp(1.0, -cs11);
+    std::vector<double> R((size_t)1 << B);
+    R[0] = 0.0;
+    for (int i = 0; i < B; ++i) {
+      const double qiB = q[(size_t)i * n + B];
+      for (int z = 0; z < (1 << i); ++z) R[z + (1 << i)] = R[z] + qiB;
+    }
+    const double qBB = q[(size_t)B * n + B];
+    auto t11 = [&](int z11) {
+      const int z = z11 & ((1 << B) - 1);
+      const double t = (double)P.T[z] + ((z11 >> B) ? qBB + R[z] : 0.0);
+      return (int)std::nearbyint(t * sc11);
+    };
+    pl.imm2_words.assign((size_t)1 << B, 0u);
+    for (int z11 = 0; z11 < (2 << B); z11 += 2)
+      pl.imm2_words[z11 / 2] = (unsigned)(t11(z11) + bias) | ((unsigned)(t11(z11 + 1) + bias) << 16);
+    P.coarse_shift = cs11;
+    P.coarse_scale = (float)sc11;
   }
   // coarse image for the tensor-core pass (qb_tc.cuh): D(z) = sum_i z_i hc_i + Tc(z) + beta must lie
   // in [0, 1023] (11-bit fields of the fp32 accumulators, f16-exact operands).  With
@@ -687,7 +734,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM) return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM2) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -716,17 +763,28 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const bool tc = want_tc && pl.ks->tc != nullptr;
   const bool coarse = !tc && pl.ks->coarse != nullptr &&
                       (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC || variant == QB_VARIANT_IMM ||
-                       (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
+                       variant == QB_VARIANT_IMM2 || (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   // the coarse pass with the instance's table as instruction immediates (AUTO: whenever the coarse kernel
-  // runs, unless QB_IMM=0); QB_VARIANT_COARSE forces the table-load coarse kernel
-  bool imm = coarse && (variant == QB_VARIANT_IMM || (variant == QB_VARIANT_AUTO && imm_enabled()));
+  // runs, unless QB_IMM=0); QB_VARIANT_COARSE forces the table-load coarse kernel.  Kind 2 = the 11-bit
+  // super-block kernel (needs L >= B + 2), AUTO's kind unless QB_IMM_KIND=1.
+  bool imm = coarse && (variant == QB_VARIANT_IMM || variant == QB_VARIANT_IMM2 ||
+                        (variant == QB_VARIANT_AUTO && imm_enabled()));
+  // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit kernel, reported as IMM)
+  const int imm_kind = !imm                                ? 0
+                       : variant == QB_VARIANT_IMM         ? 1
+                       : L < BMAX + 2                      ? 1
+                       : variant == QB_VARIANT_IMM2        ? 2
+                       : imm_auto_kind();
   QB_TMARK("geometry");
   // the host seed must be a value some searched state attains: whole-space searches (m_fix == 0) of the
   // coarse and tensor-core kernels, any chunk length; shards use it too (the combine treats a shard
   // that finds nothing <= the seed as empty, see the shard handling below)
   const bool seed = (coarse || tc) && m_fix == 0 && n >= 24;
-  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed)) return rc;
+  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2)) return rc;
   QB_TMARK("quantize");
+  const unsigned* imm_words = imm_kind == 2 ? pl.imm2_words.data() : pl.P->Tc2;
+  const int imm_nwords = imm_kind == 2 ? kImm2Words : kImmWords;
+  if (imm_kind == 2 && pl.imm2_words.size() != (size_t)kImm2Words) return fail(QB_E_INTERNAL, "no 11-bit coarse image");
 
   TableParams& P = *pl.P;
   P.n = n;
@@ -746,16 +804,16 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   cudaKernel_t imm_fn = nullptr;
   if (imm && variant == QB_VARIANT_AUTO) {
     const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 3.0e13 * 1e3;
-    imm = imm_auto(dev, L, imm_hash(L, P.Tc2), est_ms);
+    imm = imm_auto(dev, L, imm_hash(imm_kind, L, imm_words, imm_nwords), est_ms);
   }
   double module_ms = 0.0;
   if (imm) {
     bool loaded = false;
     const auto tm0 = std::chrono::steady_clock::now();
-    const int rc_imm = imm_kernel(dev, L, P.Tc2, &imm_fn, &loaded);
+    const int rc_imm = imm_kernel(dev, imm_kind, L, imm_words, imm_nwords, &imm_fn, &loaded);
     if (loaded) module_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
     if (int rc = rc_imm) {
-      if (variant == QB_VARIANT_IMM) return rc;
+      if (variant == QB_VARIANT_IMM || variant == QB_VARIANT_IMM2) return rc;
       imm = false;  // AUTO: the table-load coarse kernel (same results) -- reported in out->variant
     }
     QB_TMARK("imm_module");
@@ -764,7 +822,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->module_ms = module_ms;
   out->variant = fieldwalk ? QB_VARIANT_FIELDWALK
                  : tc      ? QB_VARIANT_TC
-                 : imm     ? QB_VARIANT_IMM
+                 : imm     ? (imm_kind == 2 ? QB_VARIANT_IMM2 : QB_VARIANT_IMM)
                            : (coarse ? QB_VARIANT_COARSE : QB_VARIANT_TABLE);
   out->scale_exp = pl.e;
   out->prefix_bits = pl.k;
@@ -1485,14 +1543,16 @@ int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const in
   return QB_OK;
 }
 
-int qb_imm_image(int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size) {
+int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size) {
   if (!words || !size) return qb::fail(QB_E_ARG, "null pointer");
+  if (kind != 1 && kind != 2) return qb::fail(QB_E_ARG, "kind must be 1 (10-bit) or 2 (super-block)");
   const qb_imm_cubin* cb = nullptr;
   for (const qb_imm_cubin* c = qb_imm_cubins; c->data; ++c)
-    if (c->L == L) cb = c;
+    if (c->L == L && c->kind == kind) cb = c;
   if (!cb) return qb::fail(QB_E_ARG, "no patched-immediate cubin for L=" + std::to_string(L));
   std::vector<unsigned char> img(cb->data, cb->data + cb->size);
-  if (!qb::imm_patch(img, words)) return qb::fail(QB_E_INTERNAL, "patched-immediate cubin rejected (placeholders)");
+  if (!qb::imm_patch(img, words, kind == 2 ? qb::kImm2Words : qb::kImmWords))
+    return qb::fail(QB_E_INTERNAL, "patched-immediate cubin rejected (placeholders)");
   *size = img.size();
   if (out && cap >= img.size()) std::memcpy(out, img.data(), img.size());
   return QB_OK;

@@ -1,7 +1,8 @@
-"""GPU parity of the patched-immediate coarse kernel (QB_VARIANT_IMM, AUTO's default where the coarse
-filter runs): the instance's coarse table is written into the kernel's SASS as instruction immediates
-(qb_api.cu imm_kernel / imm_patch).  Every result must equal the table-load coarse kernel's (same
-blocks, same certified bounds, same tie keys) and, where affordable, the oracle's."""
+"""GPU parity of the patched-immediate coarse kernels (QB_VARIANT_IMM: 10-bit blocks; QB_VARIANT_IMM2:
+11-bit super-blocks, AUTO's default where the coarse filter runs): the instance's coarse table is
+written into the kernel's SASS as instruction immediates (qb_api.cu imm_kernel / imm_patch).  Every
+result must equal the table-load coarse kernel's (same blocks, same certified bounds, same tie keys)
+and, where affordable, the oracle's."""
 
 import numpy as np
 import pytest
@@ -22,47 +23,54 @@ CASES = [("E", 40, 0), ("E", 40, 1), ("E", 36, 2), ("E", 33, 3), ("D", 32, 0), (
          ("B", 34, 2), ("A", 32, 5)]
 
 
+IMMS = [_lib.VARIANT_IMM, _lib.VARIANT_IMM2]
+
+
+@pytest.mark.parametrize("var", IMMS)
 @pytest.mark.parametrize("name,n,rep", CASES)
-def test_imm_equals_table_load_coarse(name, n, rep):
+def test_imm_equals_table_load_coarse(name, n, rep, var):
     c = instances.config_coeffs(name, rep, n=n)
     ref = _lib.solve(c, variant=_lib.VARIANT_COARSE)
-    got = _lib.solve(c, variant=_lib.VARIANT_IMM)
-    assert got.variant == _lib.VARIANT_IMM and ref.variant == _lib.VARIANT_COARSE
+    got = _lib.solve(c, variant=var)
+    assert got.variant in IMMS and ref.variant == _lib.VARIANT_COARSE
     assert _same(got, ref), (name, n, rep)
-    auto = _lib.solve(c)  # AUTO: this table was solved (and loaded) just above -> the patched kernel
+    auto = _lib.solve(c)  # AUTO's kind (super-blocks): loaded just above when var == IMM2
     assert _same(auto, ref)
-    if ref.variant == _lib.VARIANT_COARSE and auto.variant != _lib.VARIANT_TABLE:
-        assert auto.variant == _lib.VARIANT_IMM
+    if var == _lib.VARIANT_IMM2 and got.variant == var:
+        assert auto.variant == var
 
 
+@pytest.mark.parametrize("var", IMMS)
 @pytest.mark.parametrize("m_fix,m_tie,shards", [(0, 6, 1), (0, 0, 3), (4, 4, 1), (2, 9, 2)])
-def test_imm_subspaces_ties_and_shards(m_fix, m_tie, shards):
+def test_imm_subspaces_ties_and_shards(m_fix, m_tie, shards, var):
     """Tie-heavy integer instance (values in {-1,0,1}): subspace solves, the parallel tie rule and
     shards all agree between the two coarse kernels."""
     c = instances.int_uniform_coeffs(33, 777, -1, 1)
     for shard in range(shards):
         suffix = 3 if m_fix else 0
         ref = _lib.solve(c, m_fix, suffix, m_tie, shard=shard, shard_count=shards, variant=_lib.VARIANT_COARSE)
-        got = _lib.solve(c, m_fix, suffix, m_tie, shard=shard, shard_count=shards, variant=_lib.VARIANT_IMM)
+        got = _lib.solve(c, m_fix, suffix, m_tie, shard=shard, shard_count=shards, variant=var)
         assert _same(got, ref), (m_fix, m_tie, shard)
 
 
-def test_imm_module_cache_alternating_instances():
+@pytest.mark.parametrize("var", IMMS)
+def test_imm_module_cache_alternating_instances(var):
     """More distinct instances than the per-device module cache holds (4), solved twice in
     alternating order: every answer is the one of its own instance (cache keyed by table + L)."""
     cs = [instances.config_coeffs("E", 10 + r, n=32) for r in range(6)]
     want = [_lib.solve(c, variant=_lib.VARIANT_COARSE) for c in cs]
     for _ in range(2):
         for c, w in zip(cs, want):
-            assert _same(_lib.solve(c, variant=_lib.VARIANT_IMM), w)
+            assert _same(_lib.solve(c, variant=var), w)
 
 
-def test_imm_vs_oracle_subspace_n34():
+@pytest.mark.parametrize("var", IMMS)
+def test_imm_vs_oracle_subspace_n34(var):
     """Oracle check of an IMM search on a float instance: solve_subspace over 2^26 states."""
     c = instances.config_coeffs("E", 7, n=34)
     m, suffix = 8, 77
-    got = _lib.solve(c, m, suffix, m, variant=_lib.VARIANT_IMM)
-    assert got.variant == _lib.VARIANT_IMM
+    got = _lib.solve(c, m, suffix, m, variant=var)
+    assert got.variant in IMMS
     bits, val, _ = O.solve_subspaces(c, m, suffix, suffix + 1, threads=8)
     assert int(got.argmin_bits) == bits and got.value == val
 
@@ -73,13 +81,14 @@ def test_auto_policy_first_solve_and_repeat():
     c33 = instances.config_coeffs("E", 41, n=33)
     first = _lib.solve(c33)
     again = _lib.solve(c33)
-    assert first.variant == _lib.VARIANT_COARSE and again.variant == _lib.VARIANT_IMM
+    assert first.variant == _lib.VARIANT_COARSE and again.variant in IMMS
     assert _same(first, again)
     c40 = instances.config_coeffs("E", 42, n=40)
-    assert _lib.solve(c40).variant == _lib.VARIANT_IMM
+    assert _lib.solve(c40).variant in IMMS
 
 
-def test_imm_adversarial_ranges():
+@pytest.mark.parametrize("var", IMMS)
+def test_imm_adversarial_ranges(var):
     """Wide-range weights (one huge term, many tiny non-integer ones) and an all-zero instance."""
     n = 32
     c = np.zeros((n, n))
@@ -89,7 +98,22 @@ def test_imm_adversarial_ranges():
     c[iu] = rng.standard_normal(len(iu[0])) * 1e-3
     inst = qb.QuboInstance(c)
     ref = _lib.solve(inst.coeffs, variant=_lib.VARIANT_COARSE)
-    got = _lib.solve(inst.coeffs, variant=_lib.VARIANT_IMM)
+    got = _lib.solve(inst.coeffs, variant=var)
     assert _same(got, ref)
     z = np.zeros((n, n))
-    assert _same(_lib.solve(z, variant=_lib.VARIANT_IMM), _lib.solve(z, variant=_lib.VARIANT_COARSE))
+    assert _same(_lib.solve(z, variant=var), _lib.solve(z, variant=_lib.VARIANT_COARSE))
+
+
+def test_imm2_tie_heavy_against_oracle_full():
+    """Super-blocks on a tie-heavy integer instance (values in {-1,0,1}) at n=31: the kernel's
+    half-block keys j = 2 j' + (b ^ (j' & 1)) must reproduce the reference's global Gray-rank tie
+    rule; checked against the oracle's full solve and solve_parallel(m=5)."""
+    c = instances.int_uniform_coeffs(31, 31337, -1, 1)
+    for m_tie in (0, 5):
+        got = _lib.solve(c, 0, 0, m_tie, variant=_lib.VARIANT_IMM2)
+        assert got.variant == _lib.VARIANT_IMM2, got.prefix_bits
+        if m_tie == 0:
+            bits, val, _ = O.solve_incremental(c)
+        else:
+            bits, val, _ = O.solve_subspaces(c, m_tie, threads=8)
+        assert int(got.argmin_bits) == bits and got.value == val

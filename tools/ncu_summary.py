@@ -74,6 +74,8 @@ if record:
     lib_path = os.path.join(ROOT, "paper_2310_19373_b200", "libqubrute_b200.so")
     if fam == "coarse_kernel" and len(targs) > 6 and targs[6] in ("true", "1"):  # patched-immediate kernel (embedded cubin)
         sym, sha = imm_symbol(int(targs[4])), imm_sass_sha256(int(targs[4]))
+    elif fam == "coarse2_kernel":  # super-block patched-immediate kernel (embedded cubin)
+        sym, sha = imm_symbol(int(targs[2]), 2), imm_sass_sha256(int(targs[2]), 2)
     else:
         sym = kernel_symbol(lib_path, fam, int(targs[4]))
         sha = sass_sha256(lib_path, sym)
