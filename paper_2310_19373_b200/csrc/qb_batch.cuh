@@ -21,6 +21,11 @@
 #include "qb_table.cuh"
 #include "qb_batch_params.h"
 
+#ifndef QB_BATCH_MINB
+#define QB_BATCH_MINB 0  // 0: launch bounds on the block size only.  Measured (config C window): 86-102 regs
+                         // 0.138-0.148 ms; 64 regs (4 x 256-thread CTAs/SM) 0.158 ms; 80 regs 0.158 ms
+#endif
+
 namespace qb {
 
 __device__ __forceinline__ float2 batch_add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
@@ -87,11 +92,59 @@ __device__ __forceinline__ void batch_base(const float (*sQ)[BATCH_NMAX + 1], in
   }
 }
 
+// Append every state of block c whose value is <= theta.  Thread tid owns z = tid | (r << LB): the low
+// LB bits are fixed (their field sum is formed once), the high B - LB bits are walked in reflected
+// Gray order, so each state costs one field add, one table load and the compare (exact: integers
+// below 2^24 in fp32, any summation order).
+template <int B, int LB>
+__device__ __forceinline__ void batch_enumerate(const float* sT, const float (&H)[B], long long V, long long theta,
+                                                unsigned int c, int tid, unsigned long long* scand, int* scount) {
+  if constexpr (B <= LB) {
+    if (tid < (1 << B)) {
+      float r = sT[tid];
+#pragma unroll
+      for (int i = 0; i < B; ++i)
+        if ((tid >> i) & 1) r += H[i];
+      if (V + (long long)r <= theta) {
+        const int idx = atomicAdd(scount, 1);
+        if (idx < BATCH_CAP) scand[idx] = ((unsigned long long)c << B) | (unsigned)tid;
+      }
+    }
+  } else {
+    constexpr int HB = B - LB;
+    float lows = 0.f;
+#pragma unroll
+    for (int i = 0; i < LB; ++i)
+      if ((tid >> i) & 1) lows += H[i];
+    float hs = 0.f;
+    unsigned r = 0;
+#pragma unroll
+    for (int g = 0; g < (1 << HB); ++g) {
+      if (g) {
+        const int bit = (g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4;  // ctz(g), g < 32
+        r ^= 1u << bit;
+        hs += ((r >> bit) & 1u) ? H[LB + bit] : -H[LB + bit];
+      }
+      const unsigned z = (unsigned)tid | (r << LB);
+      const float v = sT[z] + (lows + hs);
+      if (V + (long long)v <= theta) {
+        const int idx = atomicAdd(scount, 1);
+        if (idx < BATCH_CAP) scand[idx] = ((unsigned long long)c << B) | z;
+      }
+    }
+  }
+}
+
 template <int B1, int B2>
+#if QB_BATCH_MINB > 0
+__global__ void __launch_bounds__(BATCH_TPB_MAX, QB_BATCH_MINB) batch_kernel(const BatchParams bp) {
+#else
 __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams bp) {
+#endif
   constexpr int B = B1 + B2;
   constexpr int NT = 1 << B;
   constexpr int CHUNK_CAP = 32;
+  constexpr int CHMIN_CAP = 256;
   __shared__ double sC[BATCH_NMAX][BATCH_NMAX + 1];  // folded fp64 coefficients, symmetric copy
   __shared__ float sQ[BATCH_NMAX][BATCH_NMAX + 1];   // quantized: diagonal on the diagonal, symmetric off
   __shared__ __align__(16) float sT[NT];
@@ -99,6 +152,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   __shared__ int sflag[3];                           // [0]: not integral, [1]: not exact, [2]: not finite
   __shared__ unsigned long long scand[BATCH_CAP];
   __shared__ unsigned int schunk[CHUNK_CAP];
+  __shared__ long long schmin[CHMIN_CAP];  // per-chunk block minima of the search (chunks <= CHMIN_CAP)
   __shared__ int scount, schunks;
   __shared__ Rec sbest;
   const int n = bp.n;
@@ -107,32 +161,34 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   const int lane = tid & 31, warp = tid >> 5;
 
   // ---- 0. load (folded by the host for the packed formats; folded here for the dense one) into
-  //         shared memory: one pass over global memory
+  //         shared memory: one pass over global memory.  Rows are dealt to warps and columns to
+  //         lanes (n <= 24 < 32), so no index needs an integer division.  The same pass gathers
+  //         what the quantization needs: nonzero count, integrality, r_in and the row sums.
+  const int nwarps = (nth + 31) / 32;
   if (tid == 0) { sflag[0] = sflag[1] = sflag[2] = 0; scount = 0; schunks = 0; }
   __syncthreads();
-  if (bp.fmt == BATCH_DENSE_F64) {
-    const double* C = static_cast<const double*>(bp.coeffs) + (size_t)blockIdx.x * n * n;
-    for (int idx = tid; idx < n * n; idx += nth) {
-      const int i = idx / n, j = idx % n;
-      if (j < i) continue;
-      const double a = C[idx], b = (i == j) ? 0.0 : C[j * n + i];
+  double part_rin = 0.0;
+  int nnz = 0;
+  for (int i = warp; i < n; i += nwarps) {
+    const int j = i + lane;
+    if (j >= n) continue;
+    double v;
+    if (bp.fmt == BATCH_DENSE_F64) {
+      const double* C = static_cast<const double*>(bp.coeffs) + (size_t)blockIdx.x * n * n;
+      const double a = C[i * n + j], b = (i == j) ? 0.0 : C[j * n + i];
       if (!isfinite(a) || !isfinite(b)) sflag[2] = 1;  // reported to the host as QB_E_ARG
-      const double v = (i == j) ? a : __dadd_rn(a, b);
-      sC[i][j] = v;
-      sC[j][i] = v;
-    }
-  } else {
-    for (int p = tid; p < ntri; p += nth) {
-      // row i of the packed upper triangle starts at i*n - i*(i-1)/2
-      int i = 0;
-      while ((i + 1) * n - (i + 1) * i / 2 <= p) ++i;
-      const int j = i + (p - (i * n - i * (i - 1) / 2));
-      const double v = bp.fmt == BATCH_UPPER_F32 ? (double)static_cast<const float*>(bp.coeffs)[(size_t)blockIdx.x * ntri + p]
-                                                 : static_cast<const double*>(bp.coeffs)[(size_t)blockIdx.x * ntri + p];
+      v = (i == j) ? a : __dadd_rn(a, b);
+    } else {
+      const int pidx = i * n - i * (i - 1) / 2 + (j - i);  // packed upper triangle, row-major
+      v = bp.fmt == BATCH_UPPER_F32 ? (double)static_cast<const float*>(bp.coeffs)[(size_t)blockIdx.x * ntri + pidx]
+                                    : static_cast<const double*>(bp.coeffs)[(size_t)blockIdx.x * ntri + pidx];
       if (!isfinite(v)) sflag[2] = 1;
-      sC[i][j] = v;
-      sC[j][i] = v;
     }
+    sC[i][j] = v;
+    sC[j][i] = v;
+    if (v != 0.0) ++nnz;
+    if (floor(v) != v) sflag[0] = 1;
+    if (i < B) part_rin += fabs(v);  // r_in: every upper entry in a row of the block bits
   }
   __syncthreads();
   if (sflag[2]) {  // every coefficient is read here, so the host needs no pass over the batch
@@ -141,16 +197,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   }
 
   // ---- 1. quantization: bound M = max(r_in, max row abs sum), as in qb_api.cu quantize()
-  double part_rin = 0.0, part_row = 0.0;
-  int nnz = 0;
-  for (int idx = tid; idx < n * n; idx += nth) {
-    const int i = idx / n, j = idx % n;
-    if (j < i) continue;
-    const double v = sC[i][j];
-    if (v != 0.0) ++nnz;
-    if (floor(v) != v) sflag[0] = 1;
-    if (i < B) part_rin += fabs(v);  // r_in: every upper entry in a row of the block bits
-  }
+  double part_row = 0.0;
   if (tid < n) {
     for (int j = 0; j < n; ++j) part_row += fabs(sC[tid][j]);
   }
@@ -160,7 +207,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
     if (lane == 0) sred[warp] = v;
     __syncthreads();
     double t = 0.0;
-    for (int w = 0; w < (nth + 31) / 32; ++w) t += sred[w];
+    for (int w = 0; w < nwarps; ++w) t += sred[w];
     return t;
   };
   auto block_max = [&](double v) {
@@ -169,7 +216,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
     if (lane == 0) sred[warp] = v;
     __syncthreads();
     double t = 0.0;
-    for (int w = 0; w < (nth + 31) / 32; ++w) t = fmax(t, sred[w]);
+    for (int w = 0; w < nwarps; ++w) t = fmax(t, sred[w]);
     return t;
   };
   const double r_in = block_sum(part_rin);
@@ -181,36 +228,90 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   if (!(M == 0.0 || (sflag[0] == 0 && M <= LIM))) e = (int)floor(log2(LIM / M));
   for (int guard = 0; guard < 8; ++guard) {  // retry with e-1 if rounding pushed a sum over the bound
     double prin = 0.0, prow = 0.0;
-    for (int idx = tid; idx < n * n; idx += nth) {
-      const int i = idx / n, j = idx % n;
-      const double q = nearbyint(ldexp(sC[i][j], e));
+    bool inexact = false;
+    for (int i = warp; i < n; i += nwarps) {
+      const int j = lane;
+      if (j >= n) continue;
+      const double x = ldexp(sC[i][j], e), q = nearbyint(x);
       sQ[i][j] = (float)q;
       if (j >= i && i < B) prin += fabs(q);
+      if (j >= i && x != q) inexact = true;
     }
     __syncthreads();
     if (tid < n)
       for (int j = 0; j < n; ++j) prow += fabs((double)sQ[tid][j]);
     const double ok_in = block_sum(prin), ok_row = block_max(prow);
-    if (fmax(ok_in, ok_row) <= LIM) break;
+    if (fmax(ok_in, ok_row) <= LIM) {
+      if (inexact) sflag[1] = 1;
+      break;
+    }
     --e;
   }
-  for (int idx = tid; idx < n * n; idx += nth) {
-    const int i = idx / n, j = idx % n;
-    if (j >= i && ldexp(sC[i][j], e) != (double)sQ[i][j]) sflag[1] = 1;
-  }
-  // ---- 2. inner table by doubling: T[z + 2^b] = T[z] + q_bb + sum_{i<b} z_i q_ib   (O(B) per entry)
-  if (tid == 0) sT[0] = 0.f;
   __syncthreads();
   const bool exact = sflag[1] == 0;
   const long long Eq = exact ? 0 : (long long)((nnz_all + 1.0) / 2.0) + 1;
-#pragma unroll 1
-  for (int b = 0; b < B; ++b) {
-    for (int z = tid; z < (1 << b); z += nth) {
-      float t = sT[z] + sQ[b][b];
-      for (int i = 0; i < b; ++i) t = fmaf(((z >> i) & 1) ? 1.f : 0.f, sQ[i][b], t);
-      sT[z + (1 << b)] = t;
+  // ---- 2. inner table T(z) = sum_{i<=j<B} q_ij z_i z_j
+  if constexpr (B1 == 5 && B2 == 5) {
+    // split z = (u, w), 5 bits each: T(u, w) = Tw(w) + Tu(u) + sum_{i<5} w_i G_i(u) with
+    // G_i(u) = sum_{5<=j<10} u_j q_ij.  Warp 0 fills Tw; then thread t owns row u = t & 31 and a
+    // contiguous w range, walked in reflected Gray order (one add per entry for the cross term).
+    __shared__ float sTw[32];
+    if (tid < 32) {
+      float t = 0.f;
+      for (int i = 0; i < 5; ++i) {
+        if (!((tid >> i) & 1)) continue;
+        t += sQ[i][i];
+        for (int j = i + 1; j < 5; ++j)
+          if ((tid >> j) & 1) t += sQ[i][j];
+      }
+      sTw[tid] = t;
     }
     __syncthreads();
+    const int u = tid & 31, groups = nth >> 5;  // nth in {32, 64, 128, 256}
+    const int wspan = 32 / groups, w0 = (tid >> 5) * wspan;
+    float tu = 0.f, G[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) G[i] = 0.f;
+    for (int a = 0; a < 5; ++a) {
+      if (!((u >> a) & 1)) continue;
+      tu += sQ[5 + a][5 + a];
+      for (int c2 = a + 1; c2 < 5; ++c2)
+        if ((u >> c2) & 1) tu += sQ[5 + a][5 + c2];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) G[i] += sQ[i][5 + a];
+    }
+    // cross term of the range start w0, then Gray steps over the low log2(wspan) bits of w
+    float cross = 0.f;
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+      if ((w0 >> i) & 1) cross += G[i];
+    int w = w0;
+    for (int g = 0; g < wspan; ++g) {
+      if (g) {
+        const int bit = __ffs(g) - 1;
+        w ^= 1 << bit;
+        float gi = G[0];
+#pragma unroll
+        for (int i = 1; i < 5; ++i)
+          if (bit == i) gi = G[i];
+        cross += ((w >> bit) & 1) ? gi : -gi;
+      }
+      sT[(u << 5) | w] = sTw[w] + tu + cross;
+    }
+    __syncthreads();
+  } else {
+    // doubling: T[z + 2^b] = T[z] + q_bb + sum_{i<b} z_i q_ib   (O(B) per entry; B < 10: n < 10)
+    if (tid == 0) sT[0] = 0.f;
+    __syncthreads();
+#pragma unroll 1
+    for (int b = 0; b < B; ++b) {
+      for (int z = tid; z < (1 << b); z += nth) {
+        float t = sT[z] + sQ[b][b];
+        for (int i = 0; i < b; ++i) t = fmaf(((z >> i) & 1) ? 1.f : 0.f, sQ[i][b], t);
+        sT[z + (1 << b)] = t;
+      }
+      __syncthreads();
+    }
   }
 
   // ---- 3. search
@@ -226,6 +327,7 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
     asm volatile("" : "+r"(tp));  // opaque per iteration: keeps ptxas from hoisting all 2^B table loads
     const long long val = V + (long long)batch_block_min<B1, B2>(tp, H);
     tmin = min(tmin, val);
+    if (chunks <= CHMIN_CAP) schmin[c] = val;  // the collect pass below lists from these
     const unsigned long long K = ginv64(c);  // global Gray rank >> B (one block per chunk)
     if (val < best.val || (val == best.val && K < best.K)) best = Rec{val, K, c, 0u, 0u};
   }
@@ -234,9 +336,16 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
   __syncthreads();
   const long long theta = sbest.val + 2 * Eq;
 
-  // ---- 4. certified candidates: list the chunks whose block minimum is <= theta, then the whole
-  //         CTA enumerates those blocks' states in parallel
-  if (tmin <= theta) {
+  // ---- 4. certified candidates: list the chunks whose block minimum is <= theta (from the minima
+  //         the search stored, or recomputed for more than CHMIN_CAP chunks), then the whole CTA
+  //         enumerates those blocks' states in parallel
+  if (chunks <= CHMIN_CAP) {
+    for (unsigned int c = tid; c < chunks; c += nth) {
+      if (schmin[c] > theta) continue;
+      const int idx = atomicAdd(&schunks, 1);
+      if (idx < CHUNK_CAP) schunk[idx] = c;
+    }
+  } else if (tmin <= theta) {
     for (unsigned int c = tid; c < chunks; c += nth) {
       long long V;
       float H[B];
@@ -255,15 +364,12 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
     long long V;
     float H[B];
     batch_base<B>(sQ, n, (unsigned long long)c << B, V, H);
-    for (unsigned int z = tid; z < (unsigned int)NT; z += nth) {
-      float r = sT[z];
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-        if ((z >> i) & 1u) r += H[i];
-      if (V + (long long)r <= theta) {
-        const int idx = atomicAdd(&scount, 1);
-        if (idx < BATCH_CAP) scand[idx] = ((unsigned long long)c << B) | z;
-      }
+    // thread tid owns the states z = tid + nth * r; nth is a power of two (32..256)
+    switch (nth) {
+      case 32: batch_enumerate<B, 5>(sT, H, V, theta, c, tid, scand, &scount); break;
+      case 64: batch_enumerate<B, 6>(sT, H, V, theta, c, tid, scand, &scount); break;
+      case 128: batch_enumerate<B, 7>(sT, H, V, theta, c, tid, scand, &scount); break;
+      default: batch_enumerate<B, 8>(sT, H, V, theta, c, tid, scand, &scount); break;
     }
   }
   __syncthreads();
