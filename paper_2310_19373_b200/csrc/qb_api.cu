@@ -652,6 +652,20 @@ static int choose_geometry(int n, int m_fix, int m_lock, uint32_t shard_count, i
     BE = L = std::min(lmax, BMAX);
     return QB_OK;
   }
+#ifndef QB_SMALL_CHUNKS_LOG2
+#define QB_SMALL_CHUNKS_LOG2 14  // small problems: at least 2^14 one-block chunks (fills the GPU)
+#endif
+  // small problems (n - m_fix <= 10 + QB_SMALL_CHUNKS_LOG2 on one shard): one block of 2^BE states per
+  // chunk with BE < 10, so the 2^(n - m_fix) states spread over >= 2^14 threads instead of a few SMs
+  // (config A, n = 20: 1024 ten-bit chunks would occupy 8 of 148 SMs)
+  if (!tc) {
+    const int free_bits = n - m_fix - (int)std::ceil(std::log2((double)std::max<uint32_t>(shard_count, 1)));
+    const int be_small = free_bits - QB_SMALL_CHUNKS_LOG2;
+    if (be_small < BIG_BE) {
+      BE = L = std::max(std::min(lmax, std::max(be_small, 5)), std::min(lmax, 1));
+      return QB_OK;
+    }
+  }
   BE = BIG_BE;
   // ~4 chunks per resident thread on every shard: large chunks amortise the chunk-start evaluation,
   // dynamic scheduling keeps the tail to one chunk (measured optimum on B200: n=40 -> k=20, n=32 -> k=18)

@@ -64,6 +64,16 @@ __global__ void __launch_bounds__(TPB, 2) kern(unsigned* out, unsigned seed) {
       if constexpr (K == 7) { x[i] = hmin2(x[i], x[j]); y[i] = hmin2(y[i], y[k]); }
       if constexpr (K == 8) { f[i] = fadd(f[i], f[j]); x[i] = imad(x[i], one, x[j]); }
       if constexpr (K == 9) { f[i] = fadd(f[i], f[j]); y[i] = hadd2(y[i], y[k]); }
+      // the patched-immediate coarse pass's mix: adds on the FMA-heavy pipe with an immediate table
+      // word, VIMNMX3 folds, fused VIADDMNMX with an immediate (K10: 2:1:1, K11: 2:1:2)
+      if constexpr (K == 10 || K == 11) {
+        unsigned c0, c1;
+        asm volatile("mad.lo.u32 %0, %1, %2, 0x12340001;" : "=r"(c0) : "r"(x[j]), "r"(one));
+        asm volatile("mad.lo.u32 %0, %1, %2, 0x12340002;" : "=r"(c1) : "r"(x[k]), "r"(one));
+        y[i] = vmin3(y[i], c0, c1);
+        x[i] = __viaddmin_u16x2(x[(i + 3) % CH], 0x12340003u, x[i]);
+        if constexpr (K == 11) f[i] = __uint_as_float(__viaddmin_u16x2(x[(i + 7) % CH], 0x12340004u, __float_as_uint(f[i])));
+      }
     }
   }
   unsigned acc = 0;
@@ -86,7 +96,8 @@ void run(int sms, unsigned* d, int launches) {
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  const double instr = 2.0 * CH * ITERS * (double)TPB * grid / 32.0;  // warp-instructions per launch
+  const double per_i = K == 10 ? 4.0 : K == 11 ? 5.0 : 2.0;
+  const double instr = per_i * CH * ITERS * (double)TPB * grid / 32.0;  // warp-instructions per launch
   printf("{\"kernel\": %d, \"ms_per_launch\": %.5f, \"warp_instr_per_s\": %.5e, \"sms\": %d}\n", K, ms / launches,
          instr / (ms / launches * 1e-3), sms);
 }
@@ -108,6 +119,8 @@ int main(int argc, char** argv) {
     case 7: run<7>(prop.multiProcessorCount, d, launches); break;
     case 8: run<8>(prop.multiProcessorCount, d, launches); break;
     case 9: run<9>(prop.multiProcessorCount, d, launches); break;
+    case 10: run<10>(prop.multiProcessorCount, d, launches); break;
+    case 11: run<11>(prop.multiProcessorCount, d, launches); break;
   }
   return 0;
 }

@@ -5,8 +5,9 @@ sys.path.insert(0, ROOT)
 from bench import ClockSampler  # noqa: E402
 BIN = os.path.join(ROOT, "tools", "pipe_probe")
 NAMES = ["imad+imad", "imad+vimnmx3", "imad+hadd2", "vimnmx3+hadd2", "imad+hmnmx2", "vimnmx3+hmnmx2",
-         "hadd2+hadd2", "hmnmx2+hmnmx2", "fadd+imad", "fadd+hadd2"]
-if not os.path.exists(BIN):
+         "hadd2+hadd2", "hmnmx2+hmnmx2", "fadd+imad", "fadd+hadd2", "coarse_mix_2imad_1vimnmx3_1viaddmnmx",
+         "coarse_mix_2imad_1vimnmx3_2viaddmnmx"]
+if not os.path.exists(BIN) or os.path.getmtime(BIN) < os.path.getmtime(BIN + ".cu"):
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", BIN, BIN + ".cu"])
 out = {}
 for k, name in enumerate(NAMES):
