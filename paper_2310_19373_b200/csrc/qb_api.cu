@@ -1187,7 +1187,10 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
     std::lock_guard<std::mutex> guard(dev->mu);
     const size_t ntri = (size_t)n * (n + 1) / 2;
     // pieces: the host packs piece p+1 while piece p is copied and solved
-    const int P = count >= 2048 ? 4 : (count >= 512 ? 2 : 1);
+#ifndef QB_BATCH_PIECES
+#define QB_BATCH_PIECES 2  // batches >= 2048 instances: host-pack / copy / solve pipeline depth (measured: 2 beat 4 with the warp kernel)
+#endif
+    const int P = count >= 2048 ? QB_BATCH_PIECES : (count >= 512 ? 2 : 1);
     const uint64_t per = (count + P - 1) / P;
     const size_t stage_doubles = (size_t)count * ntri;  // room for fp64 in every piece
     if (int rc = ensure(&dev->d_batch_coeffs, &dev->batch_coeffs_cap, stage_doubles)) return rc;
@@ -1210,6 +1213,11 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
     int nb = 0;
     const BatchFn* batch = batch_fns(&nb);
     if (B >= nb || !batch[B]) return fail(QB_E_INTERNAL, "no batch kernel for B=" + std::to_string(B));
+    // one warp per instance where it applies (no CTA barriers; QB_BATCH_WARP=0 selects the CTA kernel)
+    int wwarps = 0, wnmin = 0, wnmax = 0;
+    const BatchFn wfn = batch_warp_fn(&wwarps, &wnmin, &wnmax);
+    const char* wenv = std::getenv("QB_BATCH_WARP");
+    const bool use_warp = !(wenv && wenv[0] == '0') && n >= wnmin && n <= wnmax;
     int pieces = 0;
     for (int p = 0; p < P; ++p, ++pieces) {
       const uint64_t b0 = p * per, b1 = std::min<uint64_t>(count, b0 + per);
@@ -1218,7 +1226,8 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
       double* ds = dev->d_batch_coeffs + b0 * ntri;
       uint64_t bad = 0;
       const int fmt = pack_batch_piece(coeffs, n, b0, b1, hs, &bad);
-      if (fmt < 0) {
+      if (fmt < 0) {  // drain what earlier pieces enqueued before the staging buffers are reused
+        cudaStreamSynchronize(cs);
         cudaStreamSynchronize(st);
         cudaStreamSynchronize(st2);
         return fail(QB_E_ARG, "coefficients must be finite (instance " + std::to_string(bad) + ")");
@@ -1233,7 +1242,10 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
       QB_CUDA(cudaStreamWaitEvent(ks, copied, 0));
       BatchParams bp{ds, dev->d_batch_out + b0, n, (int)(b1 - b0), fmt};
       QB_CUDA(cudaEventRecord(k0, ks));
-      batch[B]<<<(unsigned)(b1 - b0), threads, 0, ks>>>(bp);
+      if (use_warp)
+        wfn<<<(unsigned)((b1 - b0 + wwarps - 1) / wwarps), 32 * wwarps, 0, ks>>>(bp);
+      else
+        batch[B]<<<(unsigned)(b1 - b0), threads, 0, ks>>>(bp);
       QB_CUDA(cudaGetLastError());
       QB_CUDA(cudaEventRecord(k1, ks));
     }

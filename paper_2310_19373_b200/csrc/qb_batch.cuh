@@ -388,13 +388,12 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
       bool have = false;
       for (int t = lane; t < cnt; t += 32) {
         const unsigned long long x = scand[t];
+        // eval_upper over the set bits only, in the reference's (i, j) order (bit-identical, see
+        // eval_upper_set_bits below)
         double acc = 0.0;
-        for (int i = 0; i < n; ++i) {
-          const double xi = (double)((x >> i) & 1ull);
-          for (int j = i; j < n; ++j) {
-            const double xj = (double)((x >> j) & 1ull);
-            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sC[i][j], xi), xj));
-          }
+        for (unsigned long long xi = x; xi; xi &= xi - 1) {
+          const int i = __ffsll((long long)xi) - 1;
+          for (unsigned long long xj = xi; xj; xj &= xj - 1) acc = __dadd_rn(acc, sC[i][__ffsll((long long)xj) - 1]);
         }
         const unsigned long long key = ginv64(x);
         if (!have || acc < bv || (acc == bv && key < bk)) { bv = acc; bx = x; bk = key; have = true; }
@@ -411,6 +410,267 @@ __global__ void __launch_bounds__(BATCH_TPB_MAX) batch_kernel(const BatchParams 
     }
     if (lane == 0) bp.out[blockIdx.x] = o;
   }
+}
+
+}  // namespace qb
+
+// ---------------------------------------------------------------------------------------------
+// Warp-per-instance batch kernel (12 <= n <= BATCHW_NMAX): the whole instance lives in one warp and
+// its slice of shared memory, so no phase needs a CTA barrier (__syncwarp only) and the 4 warps of a
+// CTA (different instances) hide each other's latencies.  Same arithmetic, tie rule and outputs as
+// batch_kernel: quantization as qb_api.cu quantize(), 5+5-bit table, one 1024-state block per chunk
+// (2^(n-10) chunks, at most 32 per lane), certified candidates re-evaluated in fp64 in eval_upper
+// order (_kernels.py:12-20), lowest (value, global Gray rank) wins (solver.py:118-136).
+namespace qb {
+
+constexpr int BATCHW_WARPS = 4;
+constexpr int BATCHW_NMAX = 17;
+constexpr int BATCHW_PER_LANE = 4;  // chunks per lane: 2^(n-10) / 32 <= 4 for n <= 17
+
+__device__ __forceinline__ int packed_row(int i, int n) { return i * n - i * (i - 1) / 2; }
+
+// eval_upper (_kernels.py:12-20) of a 0/1 vector over the packed upper triangle, adding only the terms
+// with x_i = x_j = 1, in the reference's (i, j) order.  Bit-identical to adding every term: the skipped
+// products are +-0.0, the running sum starts at +0.0 and can never become -0.0 under round-to-nearest
+// (x + (-x) = +0.0), and adding +-0.0 to any other value returns it unchanged.
+__device__ __forceinline__ double eval_upper_set_bits(const double* sCp, int n, unsigned long long x) {
+  double acc = 0.0;
+  for (unsigned long long xi = x; xi; xi &= xi - 1) {
+    const int i = __ffsll((long long)xi) - 1;
+    const double* row = sCp + packed_row(i, n) - i;  // row[j] = c_ij for j >= i
+    for (unsigned long long xj = xi; xj; xj &= xj - 1) acc = __dadd_rn(acc, row[__ffsll((long long)xj) - 1]);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(BATCHW_WARPS * 32) batch_warp_kernel(const BatchParams bp) {
+  constexpr int B1 = 5, B2 = 5, B = 10, NT = 1 << B;
+  __shared__ __align__(16) float sTa[BATCHW_WARPS][NT];
+  __shared__ float sQa[BATCHW_WARPS][BATCH_NMAX][BATCH_NMAX + 1];
+  __shared__ double sCa[BATCHW_WARPS][BATCHW_NMAX * (BATCHW_NMAX + 1) / 2];
+  __shared__ float sTwa[BATCHW_WARPS][32];
+  __shared__ unsigned long long scanda[BATCHW_WARPS][BATCH_CAP];
+  __shared__ unsigned int schunka[BATCHW_WARPS][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int inst = blockIdx.x * BATCHW_WARPS + warp;
+  if (inst >= bp.count) return;  // the whole warp leaves together
+  const unsigned FULL = 0xffffffffu;
+  float* sT = sTa[warp];
+  float (*sQ)[BATCH_NMAX + 1] = sQa[warp];
+  double* sC = sCa[warp];
+  const int n = bp.n, ntri = n * (n + 1) / 2;
+
+  // ---- 0. load (packed upper triangle; the dense fp64 format is folded here) + statistics
+  bool bad = false, nonint = false;
+  double part_rin = 0.0;
+  int nnz = 0;
+  for (int i = 0; i < n; ++i) {
+    const int j = i + lane;
+    if (j >= n) continue;
+    double v;
+    if (bp.fmt == BATCH_DENSE_F64) {
+      const double* C = static_cast<const double*>(bp.coeffs) + (size_t)inst * n * n;
+      const double a = C[i * n + j], b2 = (i == j) ? 0.0 : C[j * n + i];
+      bad |= !isfinite(a) || !isfinite(b2);
+      v = (i == j) ? a : __dadd_rn(a, b2);
+    } else {
+      const size_t pidx = (size_t)inst * ntri + packed_row(i, n) + (j - i);
+      v = bp.fmt == BATCH_UPPER_F32 ? (double)static_cast<const float*>(bp.coeffs)[pidx]
+                                    : static_cast<const double*>(bp.coeffs)[pidx];
+      bad |= !isfinite(v);
+    }
+    sC[packed_row(i, n) + (j - i)] = v;
+    if (v != 0.0) ++nnz;
+    nonint |= floor(v) != v;
+    if (i < B) part_rin += fabs(v);
+  }
+  if (__any_sync(FULL, bad)) {
+    if (lane == 0) bp.out[inst] = BatchOut{0ull, 0.0, 3, 0};
+    return;
+  }
+  __syncwarp();
+  auto cget = [&](int i, int j) { return i <= j ? sC[packed_row(i, n) + (j - i)] : sC[packed_row(j, n) + (i - j)]; };
+  auto wsum = [&](double v) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+    return v;
+  };
+  auto wmax = [&](double v) {
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+    return v;
+  };
+  // ---- 1. quantization (same rule as quantize() / batch_kernel)
+  double part_row = 0.0;
+  if (lane < n)
+    for (int j = 0; j < n; ++j) part_row += fabs(cget(lane, j));
+  const double r_in = wsum(part_rin), rmax = wmax(part_row);
+  int nnz_all = nnz;
+  for (int off = 16; off > 0; off >>= 1) nnz_all += __shfl_xor_sync(FULL, nnz_all, off);
+  const bool integral = !__any_sync(FULL, nonint);
+  const double M = fmax(r_in, rmax);
+  const double LIM = 16777215.0;
+  int e = 0;
+  if (!(M == 0.0 || (integral && M <= LIM))) e = (int)floor(log2(LIM / M));
+  bool exact = true;
+  for (int guard = 0; guard < 8; ++guard) {
+    double prin = 0.0;
+    bool inexact = false;
+    if (lane < n) {
+      for (int i = 0; i < n; ++i) {
+        const double x = ldexp(cget(i, lane), e), q = nearbyint(x);
+        sQ[i][lane] = (float)q;
+        if (lane >= i && i < B) prin += fabs(q);
+        if (lane >= i && x != q) inexact = true;
+      }
+    }
+    __syncwarp();
+    double prow = 0.0;
+    if (lane < n)
+      for (int j = 0; j < n; ++j) prow += fabs((double)sQ[lane][j]);
+    const double ok_in = wsum(prin), ok_row = wmax(prow);
+    if (fmax(ok_in, ok_row) <= LIM) {
+      exact = !__any_sync(FULL, inexact);
+      break;
+    }
+    --e;
+    __syncwarp();
+  }
+  const long long Eq = exact ? 0 : (long long)((nnz_all + 1) / 2) + 1;
+
+  // ---- 2. table: T(u, w) = Tw(w) + Tu(u) + sum_{i<5} w_i G_i(u); lane u writes row u
+  {
+    float tw = 0.f;
+    for (int i = 0; i < 5; ++i) {
+      if (!((lane >> i) & 1)) continue;
+      tw += sQ[i][i];
+      for (int j = i + 1; j < 5; ++j)
+        if ((lane >> j) & 1) tw += sQ[i][j];
+    }
+    sTwa[warp][lane] = tw;
+    const int u = lane;
+    float tu = 0.f, G[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) G[i] = 0.f;
+    for (int a = 0; a < 5; ++a) {
+      if (!((u >> a) & 1)) continue;
+      tu += sQ[5 + a][5 + a];
+      for (int c2 = a + 1; c2 < 5; ++c2)
+        if ((u >> c2) & 1) tu += sQ[5 + a][5 + c2];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) G[i] += sQ[i][5 + a];
+    }
+    __syncwarp();
+    float cross = 0.f;
+    int w = 0;
+#pragma unroll
+    for (int g = 0; g < 32; ++g) {
+      if (g) {
+        const int bit = (g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4;  // ctz(g)
+        w ^= 1 << bit;
+        cross += ((w >> bit) & 1) ? G[bit] : -G[bit];
+      }
+      sT[(u << 5) | w] = sTwa[warp][w] + tu + cross;
+    }
+  }
+  __syncwarp();
+
+  // ---- 3. search: chunk c = lane + 32 t, one 1024-state block each
+  const unsigned int chunks = 1u << (n - B);
+  long long vals[BATCHW_PER_LANE];
+  long long bestv = LLONG_MAX;
+  unsigned long long bestk = ~0ull;
+#pragma unroll
+  for (int t = 0; t < BATCHW_PER_LANE; ++t) {
+    vals[t] = LLONG_MAX;
+    const unsigned int c = (unsigned)lane + 32u * t;
+    if (c >= chunks) continue;
+    long long V;
+    float H[B];
+    batch_base<B>(sQ, n, (unsigned long long)c << B, V, H);
+    unsigned tp = (unsigned)__cvta_generic_to_shared(sT);
+    asm volatile("" : "+r"(tp));
+    const long long val = V + (long long)batch_block_min<B1, B2>(tp, H);
+    vals[t] = val;
+    const unsigned long long K = ginv64(c);
+    if (val < bestv || (val == bestv && K < bestk)) { bestv = val; bestk = K; }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const long long ov = __shfl_xor_sync(FULL, bestv, off);
+    const unsigned long long ok = __shfl_xor_sync(FULL, bestk, off);
+    if (ov < bestv || (ov == bestv && ok < bestk)) { bestv = ov; bestk = ok; }
+  }
+  const long long theta = bestv + 2 * Eq;
+
+  // ---- 4. certified candidates: blocks with minimum <= theta (ballot append), then their states
+  int nch = 0;
+#pragma unroll
+  for (int t = 0; t < BATCHW_PER_LANE; ++t) {
+    const bool hit = vals[t] <= theta;
+    const unsigned m = __ballot_sync(FULL, hit);
+    const int pos = nch + __popc(m & ((1u << lane) - 1u));
+    if (hit && pos < 32) schunka[warp][pos] = (unsigned)lane + 32u * t;
+    nch += __popc(m);
+  }
+  __syncwarp();
+  int cnt = 0;
+  if (nch <= 32) {
+    for (int t = 0; t < nch; ++t) {
+      const unsigned int c = schunka[warp][t];
+      long long V;
+      float H[B];
+      batch_base<B>(sQ, n, (unsigned long long)c << B, V, H);
+      float lows = 0.f;
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+        if ((lane >> i) & 1) lows += H[i];
+      float hs = 0.f;
+      unsigned r = 0;
+#pragma unroll
+      for (int g = 0; g < 32; ++g) {
+        if (g) {
+          const int bit = (g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4;
+          r ^= 1u << bit;
+          hs += ((r >> bit) & 1u) ? H[5 + bit] : -H[5 + bit];
+        }
+        const unsigned z = (unsigned)lane | (r << 5);
+        const bool hit = V + (long long)(sT[z] + (lows + hs)) <= theta;
+        const unsigned m = __ballot_sync(FULL, hit);
+        const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+        if (hit && pos < BATCH_CAP) scanda[warp][pos] = ((unsigned long long)c << B) | z;
+        cnt += __popc(m);
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- 5. exact re-evaluation in eval_upper order, lowest (value, global Gray rank)
+  BatchOut o{0ull, 0.0, 0, cnt};
+  if (nch > 32 || cnt > BATCH_CAP) {
+    o.status = 1;
+  } else if (cnt == 0) {
+    o.status = 2;
+  } else {
+    double bv = 0.0;
+    unsigned long long bx = 0, bk = ~0ull;
+    bool have = false;
+    if (lane < cnt) {
+      const unsigned long long x = scanda[warp][lane];
+      const double acc = eval_upper_set_bits(sC, n, x);
+      bv = acc;
+      bx = x;
+      bk = ginv64(x);
+      have = true;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(FULL, bv, off);
+      const unsigned long long ox = __shfl_xor_sync(FULL, bx, off);
+      const unsigned long long ok = __shfl_xor_sync(FULL, bk, off);
+      const int oh = __shfl_xor_sync(FULL, (int)have, off);
+      if (oh && (!have || ov < bv || (ov == bv && ok < bk))) { bv = ov; bx = ox; bk = ok; have = true; }
+    }
+    o.x = bx;
+    o.value = bv;
+  }
+  if (lane == 0) bp.out[inst] = o;
 }
 
 }  // namespace qb

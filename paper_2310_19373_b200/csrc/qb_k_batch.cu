@@ -1,4 +1,5 @@
-// Instantiations of the batch kernel (one CTA per instance), indexed by block bits B.
+// Instantiations of the batch kernels: one CTA per instance (indexed by block bits B), and the
+// warp-per-instance kernel for 12 <= n <= 17.
 #include "qb_batch.cuh"
 #include "qb_registry.h"
 
@@ -12,6 +13,13 @@ static const BatchFn kBatch[] = {nullptr,
 const BatchFn* batch_fns(int* count) {
   *count = (int)(sizeof(kBatch) / sizeof(kBatch[0]));
   return kBatch;
+}
+
+BatchFn batch_warp_fn(int* warps, int* nmin, int* nmax) {
+  *warps = BATCHW_WARPS;
+  *nmin = 12;
+  *nmax = BATCHW_NMAX;
+  return batch_warp_kernel;
 }
 
 }  // namespace qb

@@ -47,5 +47,6 @@ const LFn* coarse_fns(int* count);        // qb_k_coarse.cu
 const LFn* fieldwalk_fns(int* count);     // qb_k_fieldwalk.cu
 const LFn* tc_fns(int* count);            // qb_k_tc.cu (tensor-core coarse pass; null fin = finalize_kernel)
 const BatchFn* batch_fns(int* count);     // qb_k_batch.cu: index = block bits B (1..BMAX)
+BatchFn batch_warp_fn(int* warps, int* nmin, int* nmax);  // qb_k_batch.cu: one warp per instance
 
 }  // namespace qb

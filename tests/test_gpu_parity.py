@@ -233,7 +233,7 @@ def test_batch_rejects_non_finite():
     assert len(bits) == 64
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 9, 10, 11, 13, 16, 20])
+@pytest.mark.parametrize("n", [1, 2, 5, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 20])
 def test_batch_ties_and_sizes(n):
     count = 40
     batch = np.stack([_tie_heavy(n, 77 * n + b, -1, 1) for b in range(count)])
@@ -594,3 +594,18 @@ def test_batch_across_devices_gathers_in_order(golden, devices):
     mins, mvals = qb.solve_batch(batch[:5], as_arrays=True, devices=devices + [0, 0, 0, 0])
     assert [qb.bits_to_int(m) for m in mins] == cb["bits"][:5]
     assert mvals.tolist() == cb["values"][:5]
+
+
+@pytest.mark.parametrize("n", [12, 14, 16, 17])
+def test_batch_warp_kernel_equals_cta_kernel(n, monkeypatch):
+    """The warp-per-instance batch kernel (12 <= n <= 17) against the one-CTA-per-instance kernel
+    (QB_BATCH_WARP=0) on float, integer and tie-heavy instances, fp32- and fp64-packed inputs."""
+    batch = np.stack([instances.normal_coeffs(n, 7000 + b) for b in range(300)]
+                     + [instances.int_uniform_coeffs(n, 8000 + b, -3, 3) for b in range(100)]
+                     + [_tie_heavy(n, 9000 + b, -1, 1) for b in range(60)])
+    batch[333, 1, 2] += 0.1  # one piece ships fp64
+    got = _lib.solve_batch(batch)
+    monkeypatch.setenv("QB_BATCH_WARP", "0")
+    ref = _lib.solve_batch(batch)
+    assert [int(b) for b in got[0]] == [int(b) for b in ref[0]]
+    assert got[1].tolist() == ref[1].tolist()
