@@ -50,7 +50,9 @@ extern "C" {
 #define QB_VARIANT_IMM 5       /* coarse kernel with the instance's coarse table patched into its SASS as
                                   instruction immediates (no table loads), 10-bit blocks */
 #define QB_VARIANT_IMM2 6      /* the same with 11-bit coarse super-blocks (two blocks per coarse pass, chunks
-                                  of >= 12 free bits); AUTO's choice where COARSE runs */
+                                  of >= 12 free bits) */
+#define QB_VARIANT_IMM8 7      /* patched-immediate threshold pass: four states per register as bytes whose top
+                                  bit says "above the pruning limit", folded by LOP3 (qb_coarse8.cuh) */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {
@@ -152,7 +154,7 @@ int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_
                    double* fields);
 
 /* Test hook (host only): the embedded patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 512 coarse
- * table words; 2: QB_VARIANT_IMM2, 1024 words) for chunk length L with `words` written into its
+ * table words; 2: QB_VARIANT_IMM2, 1024 words; 3: QB_VARIANT_IMM8, 256 words) for chunk length L with `words` written into its
  * placeholder immediates -- the image those variants load.
  * *size receives the image size; the image is copied to `out` when cap >= *size. */
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);

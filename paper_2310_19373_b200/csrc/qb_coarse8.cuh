@@ -1,0 +1,171 @@
+// Byte-packed threshold kernel (QB_VARIANT_IMM8): the patched-immediate coarse pass with FOUR states
+// per 32-bit register.
+//
+// Same chunks, outer Gray walk, blocks, tie keys, exact re-evaluation and records as coarse_kernel
+// (qb_coarse.cuh).  What changes is the coarse test of a 1024-state block.  The 16-bit pass forms the
+// block's coarse MINIMUM (two states per register, packed u16 min) and compares it with the pruning
+// limit.  The only thing the search needs from it is the comparison, so this pass forms, for every
+// state z of the block, the byte
+//
+//     f(z) = base + sum_{i in z} hc_i + Tc8(z),     base = 127 - Lc
+//
+// where hc_i = rint(H_i 2^-s8), Tc8(z) = rint(T(z) 2^-s8) (coarse unit 2^s8 quantized units) and Lc is the
+// block's own limit in coarse units, Lc = floor((lim - V) / 2^s8): bit 7 of f(z) is CLEAR exactly when the
+// state's coarse value is <= the limit.  Four states share a register (w = 4q .. 4q+3), the adds are
+// plain 32-bit adds, and one LOP3 ANDs two result registers into an accumulator: the block holds a
+// state under the limit iff some byte of the AND has bit 7 clear.  Every state's coarse value is
+// still formed and tested -- one add per four states plus half a LOP3, against one add per two states
+// plus a packed min in the 16-bit pass.
+//
+// Range (host, quantize(): c8_rneg / the choice of s8): with X(z) = sum hc_i z_i + Tc8(z) in [-Rneg, Rpos]
+// over every state and every reachable field vector, and Rneg + Rpos <= 127, the limit is clamped to
+// Lc in [-Rneg - 1, -1].  Lc >= 0 means z = 0 (coarse value 0) is under the limit: the block is
+// re-evaluated without looking at the bytes.  Lc < -Rneg - 1 means no state can be under it, and the
+// clamped test (nothing <= -Rneg - 1) says the same.  So base lies in [128, 128 + Rneg], every byte in
+// [128 - Rneg, 128 + Rneg + Rpos] = [1, 255]: no byte ever wraps or carries into its neighbour, and adding
+// a replicated or packed signed constant modulo 2^32 adds it to every byte exactly.
+//
+// Certified bound: as in the 16-bit pass, exact(z) >= V + (C(z) - (B+1)/2) 2^s8, and lim = thr + slack
+// (+ 2 Eq on the recording search, see below), so a block with no byte under the limit holds neither a
+// better state nor a tie.  Rows u (4 bits) run in reflected Gray order; a row's A_u (replicated in the
+// four bytes) is either added by a 3-input IADD3 together with the table immediate (ALU pipe) or by two
+// IMADs (FMA-heavy pipe): QB_IMM8_LAZY of the 16 registers of a row take the IADD3 form so that the two
+// integer pipes carry equal work (the LOP3 folds are ALU work as well).
+//
+// Recording search (MODE_SEARCH_RECORD, the certified collect path): the 16-bit kernel records a lower
+// bound for each pruned block.  This pass has no block minimum to record; instead its limit includes
+// the collect margin (lim = thr + slack + theta_add), so a pruned block holds no state within theta_add
+// of any value attained so far -- in particular none within theta_add of the final minimum -- and
+// contributes nothing to the chunk minimum.
+#pragma once
+#include "qb_coarse.cuh"
+
+#ifndef QB_IMM8_LAZY
+#define QB_IMM8_LAZY 9  // of the 16 registers of a row, those whose A_u + table add is one IADD3 (ALU pipe); measured n=40: 8: 25.4, 9: 22.7, 10: 23.2, 11: 23.1, 12: 24.2 ms
+#endif
+#ifndef QB_IMM8_MINB
+#define QB_IMM8_MINB 4
+#endif
+
+namespace qb {
+
+// a + b on the FMA-heavy pipe (IMAD with an opaque multiplier of 1), both operands in registers
+__device__ __forceinline__ unsigned add_fma_reg(unsigned a, unsigned one, unsigned b) {
+  unsigned r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+}
+
+// AND of the 2^B bytes f(z) of a block (four per register); see the file header.
+template <int CB1, int CB2>
+__device__ __forceinline__ unsigned coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2], int base) {
+  constexpr int B = CB1 + CB2, NU = 1 << CB1, NQ = 1 << (CB2 - 2);
+  static_assert(CB2 >= 3 && CB1 >= 1 && CB1 <= 5, "four w states per register, at least two registers per row");
+  int hc[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) hc[i] = __float2int_rn(H[i] * p.c8_scale);
+  // X4[q] byte j = base + sum_{i in w} hc_i, w = 4q + j
+  unsigned X4[NQ];
+  X4[0] = (unsigned)base * 0x01010101u + (unsigned)hc[0] * 0x01000100u + (unsigned)hc[1] * 0x01010000u;
+#pragma unroll
+  for (int i = 2; i < CB2; ++i) {
+    const unsigned d = (unsigned)hc[i] * 0x01010101u;
+#pragma unroll
+    for (int m = 0; m < (1 << (i - 2)); ++m) X4[m + (1 << (i - 2))] = X4[m] + d;
+  }
+  unsigned du[CB1];
+#pragma unroll
+  for (int i = 0; i < CB1; ++i) du[i] = (unsigned)hc[CB2 + i] * 0x01010101u;
+  const unsigned one = p.imm_one;
+  unsigned a4 = 0u;
+  unsigned acc[2] = {0xffffffffu, 0xffffffffu};
+#pragma unroll
+  for (int g = 0; g < NU; ++g) {
+    const int u = g ^ (g >> 1);
+    if (g) {
+      const int i = (g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4;  // ctz(g), g < 32
+      a4 = ((u >> i) & 1) ? a4 + du[i] : a4 - du[i];
+    }
+    const unsigned ph = QB_IMM_PH | (unsigned)(u * NQ);
+    unsigned r[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const bool lazy = ((q + 1) * QB_IMM8_LAZY) / NQ > (q * QB_IMM8_LAZY) / NQ;
+      if (g == 0) r[q] = add_fma_pipe(X4[q], one, ph | q);             // A_0 = 0
+      else if (lazy) r[q] = X4[q] + a4 + (ph | (unsigned)q);           // IADD3 (ALU pipe)
+      else r[q] = add_fma_pipe(add_fma_reg(X4[q], one, a4), one, ph | q);  // two IMADs (FMA-heavy pipe)
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; q += 2) acc[(q >> 1) & 1] &= r[q] & r[q + 1];
+  }
+  return acc[0] & acc[1];
+}
+
+template <int B1, int B2, int CB1, int CB2, int L, int TPB>
+__global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2;
+  static_assert(CB1 + CB2 == B, "coarse split must cover the table bits");
+  constexpr int LO = L - B;
+  constexpr int NF = (L - B) > 0 ? (L - B) : 1;
+  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+  const int lane = threadIdx.x & 31;
+  // (B+1)/2 coarse units, quantized; the recording search adds the collect margin (file header)
+  const long long slack = ((long long)(B + 1) << p.c8_shift >> 1) + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);
+  const int sh = p.c8_shift;
+  const long long lc_min = -(long long)p.c8_rneg - 1;
+
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(p.work, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= nchunks) break;
+    const unsigned long long ci = base + lane;
+    if (ci >= nchunks) continue;
+    const unsigned long long c = p.chunk_begin + ci;
+    const unsigned long long s = chunk_prefix(p, c);
+    long long V;
+    float H[B], F[NF];
+    {
+      ChunkStart<B, NF> cs0 = chunk_start_ool<B, L>(p, s);
+      V = cs0.V;
+#pragma unroll
+      for (int i = 0; i < B; ++i) H[i] = cs0.H[i];
+#pragma unroll
+      for (int m = 0; m < NF; ++m) F[m] = cs0.F[m];
+    }
+    int dir;
+    const unsigned long long key_hi = chunk_key(p, s, dir);
+    long long cmin = LLONG_MAX;
+    long long thr = min(min(best.val, gbest_dec(__ldcg(p.gbest))), p.seed_val);
+    for (unsigned int j = 0; j < (1u << LO); ++j) {
+      if (j) {
+        const int r = __ffs(j) - 1;
+        const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
+        outer_flip<B, L, B>(p, B + r, sg, V, H, F);
+      }
+      if constexpr (LO <= 6) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+      // the block's limit in coarse units relative to its base (floor); no limit yet: everything passes
+      const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
+      const int lc = (int)min(max(lrel, lc_min), -1ll);
+      const unsigned a = coarse8_block_and<CB1, CB2>(p, H, 127 - lc);
+      if (lrel < 0 && (a & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
+      const long long val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
+      cmin = min(cmin, val);
+      if (val <= best.val) {
+        const unsigned long long K = block_key(p, key_hi, dir, j, LO);
+        if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
+        if (val < thr) {
+          thr = val;
+          atomicMax(p.gbest, gbest_enc(val));
+        }
+      }
+    }
+    if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
+  }
+  // records only: the reduction runs as finalize_kernel (qb_table.cuh)
+  const Rec r = cta_reduce<TPB>(best);
+  if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
+}
+
+}  // namespace qb

@@ -102,6 +102,12 @@ struct alignas(16) TableParams {
   unsigned long long list_cap;
   const double* coeffs64;          // original fp64 coefficients (device), for the overflow reduction
   unsigned long long* red;         // [0] best ordered value, [1] best tie key (overflow reduction)
+  // byte-packed threshold pass (qb_coarse8.cuh): coarse unit 2^c8_shift quantized units, and the bound
+  // Rneg on how far below its base a block's coarse values can reach (limits are clamped at -Rneg - 1)
+  float c8_scale;
+  int c8_shift;
+  int c8_rneg;
+  int c8_pad;
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };
