@@ -231,7 +231,7 @@ static int ensure_host(T** ptr, size_t* cap, size_t need) {
 extern "C" {
 struct qb_imm_cubin {
   int kind;  // 1: coarse_kernel<.., IMM = true> (10-bit pass), 2: coarse2_kernel (11-bit super-blocks),
-             // 3: coarse8_kernel (byte-packed threshold pass)
+             // 3: coarse8_kernel (byte-packed threshold pass), 4: coarse8s_kernel (its super-block form)
   int L;
   const unsigned char* data;
   size_t size;
@@ -243,6 +243,7 @@ namespace qb {
 constexpr int kImmWords = 1 << (BMAX - 1);  // Tc2 words = placeholders of the 10-bit kernel
 constexpr int kImm2Words = 1 << BMAX;       // Tc11 words = placeholders of the super-block kernel
 constexpr int kImm8Words = 1 << (BMAX - 2);  // byte-packed words = placeholders of the threshold kernel
+constexpr int kImm8sWords = 1 << (BMAX - 1);  // ... of its super-block form (11 image bits)
 
 // Write words[idx] into every SASS instruction whose 32-bit immediate (bits 32..63 of the first
 // instruction word) is QB_IMM_PH | idx, in every .text section.  Each placeholder must occur exactly
@@ -290,6 +291,10 @@ static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words, in
 }
 
 static std::string imm_kernel_name(int kind, int L) {
+  if (kind == 4)
+    return "_ZN2qb15coarse8s_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
+           std::to_string(QB_COARSE_B1) + "ELi" + std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" +
+           std::to_string(TPB) + "EEEvNS_11TableParamsE";
   if (kind == 3)
     return "_ZN2qb14coarse8_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
            std::to_string(QB_COARSE_B1) + "ELi" + std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" +
@@ -446,7 +451,7 @@ static double sym(const double* c, int n, int i, int j) {
 static long long seed_greedy(const std::vector<double>& q, int n);
 
 static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false, bool seed = false,
-                    bool imm2_image = false, bool imm8_image = false) {
+                    bool imm2_image = false, int imm8_image = 0) {
   const double LIM = 16777215.0;  // 2^24 - 1
   auto bound = [&](auto get) {
     double r_in = 0.0, rmax = 0.0;
@@ -577,24 +582,40 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
   P.c8_shift = 0;
   P.c8_rneg = 0;
   P.c8_pad = 0;
-  if (imm8_image && B == BMAX) {
-    // byte image of the threshold kernel (qb_coarse8.cuh).  H_i = sum_{q >= B} x_q q_iq lies in
-    // [hneg_i, hpos_i] for every state, rint is monotone and the device forms H_i 2^-s exactly, so
-    // hc_i lies in [rint(hneg_i 2^-s), rint(hpos_i 2^-s)].  X(z) = sum_{i in z} hc_i + Tc8(z) is bounded over the
-    // 2^B inner states by doubling; s8 is the smallest shift with Rneg + Rpos <= 127.
-    double hpos[BMAX], hneg[BMAX];
-    for (int i = 0; i < B; ++i) {
+  if (imm8_image && B == BMAX && (imm8_image == 1 || n > B)) {
+    // byte image of the threshold kernels (qb_coarse8.cuh); imm8_image == 2: the super-block form, whose
+    // image also covers bit B (NB = B + 1 image bits, fields formed from the bits above B only).
+    // H_i = sum_{q >= NB} x_q q_iq lies in [hneg_i, hpos_i] for every state, rint is monotone and the device
+    // forms H_i 2^-s exactly, so hc_i lies in [rint(hneg_i 2^-s), rint(hpos_i 2^-s)].
+    // X(z) = sum_{i in z} hc_i + Tc8(z) is bounded over the 2^NB image states by doubling; s8 is the smallest
+    // shift with Rneg + Rpos <= 127.
+    const int NB = imm8_image == 2 ? B + 1 : B;
+    double hpos[BMAX + 1], hneg[BMAX + 1];
+    for (int i = 0; i < NB; ++i) {
       hpos[i] = hneg[i] = 0.0;
-      for (int q2 = B; q2 < n; ++q2) {
+      for (int q2 = NB; q2 < n; ++q2) {
         const double v = i < q2 ? q[(size_t)i * n + q2] : q[(size_t)q2 * n + i];
         (v > 0 ? hpos[i] : hneg[i]) += v;
       }
     }
-    std::vector<int> tc8((size_t)1 << B), up((size_t)1 << B), dn((size_t)1 << B);
+    // image table over NB bits: T(z), and for the super-block T(z) + b (q_BB + sum_{i<B} z_i q_iB)
+    std::vector<double> timg((size_t)1 << NB);
+    for (int z = 0; z < (1 << B); ++z) timg[z] = (double)P.T[z];
+    if (NB > B) {
+      std::vector<double> RB((size_t)1 << B);
+      RB[0] = 0.0;
+      for (int i = 0; i < B; ++i) {
+        const double qiB = q[(size_t)i * n + B];
+        for (int z = 0; z < (1 << i); ++z) RB[z + (1 << i)] = RB[z] + qiB;
+      }
+      const double qBB = q[(size_t)B * n + B];
+      for (int z = 0; z < (1 << B); ++z) timg[(size_t)z + (1 << B)] = (double)P.T[z] + qBB + RB[z];
+    }
+    std::vector<int> tc8((size_t)1 << NB), up((size_t)1 << NB), dn((size_t)1 << NB);
     for (int s8 = 0; s8 <= 60; ++s8) {
       const double sc8 = std::ldexp(1.0, -s8);
       up[0] = dn[0] = 0;
-      for (int i = 0; i < B; ++i) {
+      for (int i = 0; i < NB; ++i) {
         const int cp = (int)std::nearbyint(hpos[i] * sc8), cn = (int)std::nearbyint(hneg[i] * sc8);
         for (int z = 0; z < (1 << i); ++z) {
           up[z + (1 << i)] = up[z] + cp;
@@ -603,8 +624,8 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
       }
       bool fits = true;
       int rpos = 0, rneg = 0;
-      for (int z = 0; z < (1 << B) && fits; ++z) {
-        const double t = std::nearbyint((double)P.T[z] * sc8);
+      for (int z = 0; z < (1 << NB); ++z) {
+        const double t = std::nearbyint(timg[z] * sc8);
         if (std::fabs(t) > 127.0) { fits = false; break; }
         tc8[z] = (int)t;
         rpos = std::max(rpos, up[z] + tc8[z]);
@@ -614,9 +635,9 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
       P.c8_shift = s8;
       P.c8_scale = (float)sc8;
       P.c8_rneg = rneg;
-      // word u * 16 + q: bytes j = 0..3 hold Tc8(z), z = (u << 6) | (4 q + j); signed bytes summed modulo 2^32
-      pl.imm8_words.assign((size_t)1 << (B - 2), 0u);
-      for (int z = 0; z < (1 << B); ++z)
+      // word z >> 2 = u * 16 + q: bytes j = 0..3 hold Tc8(z), z = (u << 6) | (4 q + j); signed bytes summed mod 2^32
+      pl.imm8_words.assign((size_t)1 << (NB - 2), 0u);
+      for (int z = 0; z < (1 << NB); ++z)
         pl.imm8_words[z >> 2] += (unsigned)tc8[z] << (8 * (z & 3));
       break;
     }
@@ -804,7 +825,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8) return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8S) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -833,34 +854,38 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const bool tc = want_tc && pl.ks->tc != nullptr;
   const bool coarse = !tc && pl.ks->coarse != nullptr &&
                       (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC || variant == QB_VARIANT_IMM ||
-                       variant == QB_VARIANT_IMM2 || variant == QB_VARIANT_IMM8 ||
+                       variant == QB_VARIANT_IMM2 || variant == QB_VARIANT_IMM8 || variant == QB_VARIANT_IMM8S ||
                        (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   // the coarse pass with the instance's table as instruction immediates (AUTO: whenever the coarse kernel
   // runs, unless QB_IMM=0); QB_VARIANT_COARSE forces the table-load coarse kernel.  Kind 2 = the 11-bit
   // super-block kernel (needs L >= B + 2), AUTO's kind unless QB_IMM_KIND=1.
   bool imm = coarse && (variant == QB_VARIANT_IMM || variant == QB_VARIANT_IMM2 || variant == QB_VARIANT_IMM8 ||
+                        variant == QB_VARIANT_IMM8S ||
                         (variant == QB_VARIANT_AUTO && imm_enabled()));
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit kernel, reported as IMM)
   int imm_kind = !imm                                ? 0
                  : variant == QB_VARIANT_IMM         ? 1
                  : variant == QB_VARIANT_IMM8        ? 3
+                 : variant == QB_VARIANT_IMM8S       ? 4
                  : variant == QB_VARIANT_AUTO        ? imm_auto_kind()
                                                      : 2;
+  // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit form of the same pass)
   if (imm_kind == 2 && L < BMAX + 2) imm_kind = 1;
+  if (imm_kind == 4 && L < BMAX + 2) imm_kind = 3;
   QB_TMARK("geometry");
   // the host seed must be a value some searched state attains: whole-space searches (m_fix == 0) of the
   // coarse and tensor-core kernels, any chunk length; shards use it too (the combine treats a shard
   // that finds nothing <= the seed as empty, see the shard handling below)
   const bool seed = (coarse || tc) && m_fix == 0 && n >= 24;
-  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2, imm_kind == 3)) return rc;
+  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2, imm_kind == 4 ? 2 : imm_kind == 3 ? 1 : 0)) return rc;
   QB_TMARK("quantize");
-  if (imm_kind == 3 && pl.imm8_words.size() != (size_t)kImm8Words) {
+  if (imm_kind >= 3 && pl.imm8_words.size() != (size_t)(imm_kind == 4 ? kImm8sWords : kImm8Words)) {
     // no shift makes the block's coarse range fit a byte (cannot happen for finite coefficients, kept as a guard)
-    if (variant == QB_VARIANT_IMM8) return fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
+    if (variant != QB_VARIANT_AUTO) return fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
     imm_kind = 1;
   }
-  const unsigned* imm_words = imm_kind == 3 ? pl.imm8_words.data() : imm_kind == 2 ? pl.imm2_words.data() : pl.P->Tc2;
-  const int imm_nwords = imm_kind == 3 ? kImm8Words : imm_kind == 2 ? kImm2Words : kImmWords;
+  const unsigned* imm_words = imm_kind >= 3 ? pl.imm8_words.data() : imm_kind == 2 ? pl.imm2_words.data() : pl.P->Tc2;
+  const int imm_nwords = imm_kind == 4 ? kImm8sWords : imm_kind == 3 ? kImm8Words : imm_kind == 2 ? kImm2Words : kImmWords;
   if (imm_kind == 2 && pl.imm2_words.size() != (size_t)kImm2Words) return fail(QB_E_INTERNAL, "no 11-bit coarse image");
 
   TableParams& P = *pl.P;
@@ -890,7 +915,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     const int rc_imm = imm_kernel(dev, imm_kind, L, imm_words, imm_nwords, &imm_fn, &loaded);
     if (loaded) module_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
     if (int rc = rc_imm) {
-      if (variant == QB_VARIANT_IMM || variant == QB_VARIANT_IMM2 || variant == QB_VARIANT_IMM8) return rc;
+      if (variant != QB_VARIANT_AUTO) return rc;
       imm = false;  // AUTO: the table-load coarse kernel (same results) -- reported in out->variant
     }
     QB_TMARK("imm_module");
@@ -899,7 +924,10 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->module_ms = module_ms;
   out->variant = fieldwalk ? QB_VARIANT_FIELDWALK
                  : tc      ? QB_VARIANT_TC
-                 : imm     ? (imm_kind == 3 ? QB_VARIANT_IMM8 : imm_kind == 2 ? QB_VARIANT_IMM2 : QB_VARIANT_IMM)
+                 : imm     ? (imm_kind == 4   ? QB_VARIANT_IMM8S
+                              : imm_kind == 3 ? QB_VARIANT_IMM8
+                              : imm_kind == 2 ? QB_VARIANT_IMM2
+                                              : QB_VARIANT_IMM)
                            : (coarse ? QB_VARIANT_COARSE : QB_VARIANT_TABLE);
   out->scale_exp = pl.e;
   out->prefix_bits = pl.k;
@@ -1648,13 +1676,14 @@ int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const in
 
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size) {
   if (!words || !size) return qb::fail(QB_E_ARG, "null pointer");
-  if (kind < 1 || kind > 3) return qb::fail(QB_E_ARG, "kind must be 1 (10-bit), 2 (super-block) or 3 (byte-packed)");
+  if (kind < 1 || kind > 4)
+    return qb::fail(QB_E_ARG, "kind must be 1 (10-bit), 2 (super-block), 3 (byte-packed) or 4 (byte-packed super-block)");
   const qb_imm_cubin* cb = nullptr;
   for (const qb_imm_cubin* c = qb_imm_cubins; c->data; ++c)
     if (c->L == L && c->kind == kind) cb = c;
   if (!cb) return qb::fail(QB_E_ARG, "no patched-immediate cubin for L=" + std::to_string(L));
   std::vector<unsigned char> img(cb->data, cb->data + cb->size);
-  if (!qb::imm_patch(img, words, kind == 3 ? qb::kImm8Words : kind == 2 ? qb::kImm2Words : qb::kImmWords))
+  if (!qb::imm_patch(img, words, kind == 4 ? qb::kImm8sWords : kind == 3 ? qb::kImm8Words : kind == 2 ? qb::kImm2Words : qb::kImmWords))
     return qb::fail(QB_E_INTERNAL, "patched-immediate cubin rejected (placeholders)");
   *size = img.size();
   if (out && cap >= img.size()) std::memcpy(out, img.data(), img.size());

@@ -56,11 +56,14 @@ __device__ __forceinline__ unsigned add_fma_reg(unsigned a, unsigned one, unsign
   return r;
 }
 
-// AND of the 2^B bytes f(z) of a block (four per register); see the file header.
-template <int CB1, int CB2>
-__device__ __forceinline__ unsigned coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2], int base) {
-  constexpr int B = CB1 + CB2, NU = 1 << CB1, NQ = 1 << (CB2 - 2);
-  static_assert(CB2 >= 3 && CB1 >= 1 && CB1 <= 5, "four w states per register, at least two registers per row");
+// AND of the bytes f(z) of a block (four per register); see the file header.  SUPER: the rows also run
+// over one more bit (the first outer bit, field hcx = rint(F_B 2^-s8)): 32 rows, the first 16 of the Gray
+// walk are the block with that bit 0 (out[0]), the last 16 the block with it 1 (out[1]).
+template <int CB1, int CB2, bool SUPER>
+__device__ __forceinline__ void coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2], float FB, int base,
+                                                  unsigned (&out)[2]) {
+  constexpr int B = CB1 + CB2, UB = CB1 + (SUPER ? 1 : 0), NU = 1 << UB, NQ = 1 << (CB2 - 2);
+  static_assert(CB2 >= 3 && CB1 >= 1 && UB <= 5, "four w states per register, at least two registers per row");
   int hc[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) hc[i] = __float2int_rn(H[i] * p.c8_scale);
@@ -73,15 +76,17 @@ __device__ __forceinline__ unsigned coarse8_block_and(const TableParams& p, cons
 #pragma unroll
     for (int m = 0; m < (1 << (i - 2)); ++m) X4[m + (1 << (i - 2))] = X4[m] + d;
   }
-  unsigned du[CB1];
+  unsigned du[UB];
 #pragma unroll
   for (int i = 0; i < CB1; ++i) du[i] = (unsigned)hc[CB2 + i] * 0x01010101u;
+  if constexpr (SUPER) du[CB1] = (unsigned)__float2int_rn(FB * p.c8_scale) * 0x01010101u;
   const unsigned one = p.imm_one;
   unsigned a4 = 0u;
-  unsigned acc[2] = {0xffffffffu, 0xffffffffu};
+  unsigned acc[2][2] = {{0xffffffffu, 0xffffffffu}, {0xffffffffu, 0xffffffffu}};
 #pragma unroll
   for (int g = 0; g < NU; ++g) {
     const int u = g ^ (g >> 1);
+    const int half = SUPER ? (g >> CB1) : 0;  // reflected Gray order: the top row bit is 0 for the first half
     if (g) {
       const int i = (g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4;  // ctz(g), g < 32
       a4 = ((u >> i) & 1) ? a4 + du[i] : a4 - du[i];
@@ -96,9 +101,10 @@ __device__ __forceinline__ unsigned coarse8_block_and(const TableParams& p, cons
       else r[q] = add_fma_pipe(add_fma_reg(X4[q], one, a4), one, ph | q);  // two IMADs (FMA-heavy pipe)
     }
 #pragma unroll
-    for (int q = 0; q < NQ; q += 2) acc[(q >> 1) & 1] &= r[q] & r[q + 1];
+    for (int q = 0; q < NQ; q += 2) acc[half][(q >> 1) & 1] &= r[q] & r[q + 1];
   }
-  return acc[0] & acc[1];
+  out[0] = acc[0][0] & acc[0][1];
+  out[1] = acc[1][0] & acc[1][1];
 }
 
 template <int B1, int B2, int CB1, int CB2, int L, int TPB>
@@ -148,8 +154,9 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
       // the block's limit in coarse units relative to its base (floor); no limit yet: everything passes
       const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
       const int lc = (int)min(max(lrel, lc_min), -1ll);
-      const unsigned a = coarse8_block_and<CB1, CB2>(p, H, 127 - lc);
-      if (lrel < 0 && (a & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
+      unsigned a[2];
+      coarse8_block_and<CB1, CB2, false>(p, H, 0.f, 127 - lc, a);
+      if (lrel < 0 && (a[0] & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
       const long long val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
       cmin = min(cmin, val);
       if (val <= best.val) {
@@ -164,6 +171,90 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
   }
   // records only: the reduction runs as finalize_kernel (qb_table.cuh)
+  const Rec r = cta_reduce<TPB>(best);
+  if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
+}
+
+// Super-block form (QB_VARIANT_IMM8S): the byte image also covers the first outer bit B, as in
+// coarse2_kernel (qb_coarse2.cuh): one pass tests the two blocks that differ only in bit B against the
+// same limit (relative to the base V of the half with bit B = 0), the outer Gray walk runs over bits
+// B+1 .. L-1, and each half that holds a byte under the limit is re-evaluated exactly from its own base,
+// in original block order j = 2 j' + (b ^ (j' & 1)), so keys, records and finalize_kernel see the
+// blocks of the 10-bit walk.  Certified bound: (11 + 1)/2 coarse units.
+template <int B1, int B2, int CB1, int CB2, int L, int TPB>
+__global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __grid_constant__ TableParams p) {
+  constexpr int B = B1 + B2;
+  static_assert(CB1 + CB2 == B && B == BMAX, "super-blocks extend the 10-bit table blocks");
+  static_assert(L >= B + 2, "needs at least one walked outer bit besides bit B");
+  constexpr int LO = L - B;   // outer bits of the 10-bit walk (block index j has LO bits)
+  constexpr int LS = LO - 1;  // walked bits B+1 .. L-1 (super-block index j')
+  constexpr int NF = LO;
+  Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
+  const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
+  const int lane = threadIdx.x & 31;
+  const long long slack = ((long long)(B + 2) << p.c8_shift >> 1) + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);
+  const int sh = p.c8_shift;
+  const long long lc_min = -(long long)p.c8_rneg - 1;
+
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(p.work, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= nchunks) break;
+    const unsigned long long ci = base + lane;
+    if (ci >= nchunks) continue;
+    const unsigned long long c = p.chunk_begin + ci;
+    const unsigned long long s = chunk_prefix(p, c);
+    long long V;
+    float H[B], F[NF];
+    {
+      ChunkStart<B, NF> cs0 = chunk_start_ool<B, L>(p, s);
+      V = cs0.V;
+#pragma unroll
+      for (int i = 0; i < B; ++i) H[i] = cs0.H[i];
+#pragma unroll
+      for (int m = 0; m < NF; ++m) F[m] = cs0.F[m];
+    }
+    int dir;
+    const unsigned long long key_hi = chunk_key(p, s, dir);
+    long long cmin = LLONG_MAX;
+    long long thr = min(min(best.val, gbest_dec(__ldcg(p.gbest))), p.seed_val);
+    for (unsigned int jp = 0; jp < (1u << LS); ++jp) {
+      if (jp) {
+        const int r = __ffs(jp) - 1;
+        const float sg = ((jp >> (r + 1)) & 1u) ? -1.f : 1.f;
+        outer_flip<B, L, B + 1>(p, B + 1 + r, sg, V, H, F);
+      }
+      if constexpr (LS <= 5) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+      const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
+      const int lc = (int)min(max(lrel, lc_min), -1ll);
+      unsigned a[2];
+      coarse8_block_and<CB1, CB2, true>(p, H, F[0], 127 - lc, a);
+      if (lrel < 0 && (a[0] & a[1] & 0x80808080u) == 0x80808080u) continue;  // neither half holds a state under the limit
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {
+        const int b = t ^ (int)(jp & 1u);  // half evaluated in original block order j = 2 jp + t
+        if (lrel < 0 && ((b ? a[1] : a[0]) & 0x80808080u) == 0x80808080u) continue;
+        // exact fp32 table evaluation from the half's own base: (V, H) or (V + q_BB + F_B, H + q_.B)
+        float Hb[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) Hb[i] = b ? H[i] + p.Qs[B][i] : H[i];
+        const long long Vb = b ? V + (long long)(p.d[B] + F[0]) : V;
+        const long long val = Vb + (long long)block_min<B1, B2, 0, NF>(p, Hb, F);
+        cmin = min(cmin, val);
+        if (val <= best.val) {
+          const unsigned int j = 2u * jp + (unsigned)t;
+          const unsigned long long K = block_key(p, key_hi, dir, j, LO);
+          if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
+          if (val < thr) {
+            thr = val;
+            atomicMax(p.gbest, gbest_enc(val));
+          }
+        }
+      }
+    }
+    if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
+  }
   const Rec r = cta_reduce<TPB>(best);
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
 }
