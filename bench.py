@@ -86,8 +86,8 @@ def sass_sha256(lib_path: str, symbol: str):
 
 
 def imm_sass_sha256(L: int, kind: int = 1):
-    """sha256 of the SASS of a patched-immediate coarse kernel (kind 1: 10-bit, 2: super-block) for
-    chunk length L with its placeholders in place (the code, independent of any instance's table
+    """sha256 of the SASS of a patched-immediate coarse kernel (kind 1: 10-bit, 2: super-block, 3: byte-packed
+    threshold pass, 4: its super-block form) for chunk length L with its placeholders in place (the code, independent of any instance's table
     words), or None."""
     import tempfile
 
@@ -96,7 +96,7 @@ def imm_sass_sha256(L: int, kind: int = 1):
     from paper_2310_19373_b200 import _lib
 
     try:
-        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(512 * kind, dtype=np.uint32), kind)
+        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(IMM_WORDS[kind], dtype=np.uint32), kind)
     except Exception:  # noqa: BLE001 - no cubin for this L / library without the IMM kernels
         return None
     with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
@@ -105,7 +105,13 @@ def imm_sass_sha256(L: int, kind: int = 1):
         return sass_sha256(fh.name, imm_symbol(L, kind))
 
 
+IMM_WORDS = {1: 512, 2: 1024, 3: 256, 4: 512, 5: 256, 6: 512}  # placeholder immediates per patched kernel kind
+
+
 def imm_symbol(L: int, kind: int = 1) -> str:
+    if kind >= 3:  # byte-packed threshold kernels: 3 + super-block + 2 * row-bound form
+        fam = "15coarse8s_kernel" if kind in (4, 6) else "14coarse8_kernel"
+        return f"_ZN2qb{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}EEEvNS_11TableParamsE"
     if kind == 2:
         return f"_ZN2qb14coarse2_kernelILi5ELi5ELi{L}ELi128EEEvNS_11TableParamsE"
     return f"_ZN2qb13coarse_kernelILi5ELi5ELi4ELi6ELi{L}ELi128ELb1EEEvNS_11TableParamsE"
@@ -145,7 +151,8 @@ def fp32_lane_peak_per_sm_clk():
 
 
 FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel", 5: "coarse_kernel (imm)",
-            6: "coarse2_kernel (imm)"}
+            6: "coarse2_kernel (imm)", 7: "coarse8_kernel (imm)", 8: "coarse8s_kernel (imm)",
+            9: "coarse8_kernel (imm, row-bound)", 10: "coarse8s_kernel (imm, row-bound)"}
 
 
 def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path):
@@ -158,7 +165,7 @@ def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path)
     state's value with ~1 instruction instead of n+1 additions."""
     L = n - int(r.prefix_bits)
     family = FAMILIES.get(int(r.variant))
-    if int(r.variant) in (5, 6):  # patched-immediate kernels: SASS of the embedded cubin, placeholders in place
+    if int(r.variant) >= 5:  # patched-immediate kernels: SASS of the embedded cubin, placeholders in place
         kind = int(r.variant) - 4
         sym, sha = imm_symbol(L, kind), imm_sass_sha256(L, kind)
     else:
@@ -544,7 +551,7 @@ def main():
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max * 1e3 / args.steps},
         "gpu_launches": launches,
         "imm_module": {"load_ms": module_ms, "e2e_first_solve_of_new_table_ms": cold_ms,
-                       "note": "the patched-immediate search kernel (QB_VARIANT_IMM) is built for an instance by "
+                       "note": "the patched-immediate search kernel (QB_VARIANT_IMM*) is built for an instance by "
                                "writing its coarse table into a cubin copy and loading it (first solve of a table, "
                                "in the warm-up here); later solves of the same table reuse the loaded module, as "
                                "the timed value and e2e steps do"},
@@ -555,12 +562,14 @@ def main():
         # the other traversal kernels on the same workload: the table-load coarse kernel, the fp32 table
         # kernel and the literal per-step field walk (QB_VARIANT_COARSE / _TABLE / _FIELDWALK)
         names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse_tableload", 4: "tc", 5: "coarse_imm",
-                 6: "coarse_imm_superblock"}
+                 6: "coarse_imm_superblock", 7: "threshold_imm8", 8: "threshold_imm8_superblock", 9: "threshold_imm8_rowbound",
+                 10: "threshold_imm8_rowbound_superblock"}
         line["variants"] = {f"{names[int(r.variant)]} (default)": {
             "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
         # (the tensor-core pass, QB_VARIANT_TC, is retired from this list: 40 ms, TMEM round-trip bound,
         # DESIGN.md section 4)
-        for var in (_lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE, _lib.VARIANT_FIELDWALK):
+        for var in (_lib.VARIANT_IMM8AS, _lib.VARIANT_IMM8A, _lib.VARIANT_IMM8S, _lib.VARIANT_IMM8, _lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE,
+                    _lib.VARIANT_FIELDWALK):
             _lib.solve(inst.coeffs, variant=var)
             vr = _lib.solve(inst.coeffs, variant=var)
             vs = states / (vr.search_ms * 1e-3)

@@ -54,6 +54,9 @@ extern "C" {
 #define QB_VARIANT_IMM8 7      /* patched-immediate threshold pass: four states per register as bytes whose top
                                   bit says "above the pruning limit", folded by LOP3 (qb_coarse8.cuh) */
 #define QB_VARIANT_IMM8S 8     /* the same over 11-bit super-blocks (chunks of >= 12 free bits) */
+#define QB_VARIANT_IMM8A 9     /* row-bound form of IMM8: every row of a block is tested with the least row term
+                                  (a certified lower bound of each state), one 2-input add per four states */
+#define QB_VARIANT_IMM8AS 10   /* row-bound form of IMM8S */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {
@@ -155,7 +158,7 @@ int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_
                    double* fields);
 
 /* Test hook (host only): the embedded patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 512 coarse
- * table words; 2: QB_VARIANT_IMM2, 1024 words; 3: QB_VARIANT_IMM8, 256 words; 4: QB_VARIANT_IMM8S, 512 words) for chunk length L with `words` written into its
+ * table words; 2: QB_VARIANT_IMM2, 1024 words; 3 / 5: QB_VARIANT_IMM8 / IMM8A, 256 words; 4 / 6: QB_VARIANT_IMM8S / IMM8AS, 512 words) for chunk length L with `words` written into its
  * placeholder immediates -- the image those variants load.
  * *size receives the image size; the image is copied to `out` when cap >= *size. */
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);

@@ -29,8 +29,7 @@ IMM_LS = (10, 11, 12, 13, 14, 16, 18, 20, 22)
 IMM2_LS = (12, 13, 14, 16, 18, 20, 22)  # super-block kernel: chunks of >= B + 2 free bits
 IMM8_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse8_imm.cu")  # byte-packed threshold kernel
 IMM8_LS = IMM_LS
-IMM8S_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse8s_imm.cu")  # its 11-bit super-block form
-IMM8S_LS = IMM2_LS
+IMM8S_LS = IMM2_LS  # its 11-bit super-block form
 
 QB_OK = 0
 QB_E_ARG = -1
@@ -51,6 +50,8 @@ VARIANT_IMM = 5
 VARIANT_IMM2 = 6
 VARIANT_IMM8 = 7
 VARIANT_IMM8S = 8
+VARIANT_IMM8A = 9
+VARIANT_IMM8AS = 10
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -150,12 +151,16 @@ def build(force: bool = False, verbose: bool = False, output: str | None = None,
         procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
     cubins = []
-    for kind, src, Ls in ((1, IMM_SOURCE, IMM_LS), (2, IMM2_SOURCE, IMM2_LS), (3, IMM8_SOURCE, IMM8_LS),
-                           (4, IMM8S_SOURCE, IMM8S_LS)):
+    # kinds 3..6: byte-packed threshold kernels, 3 + super-block + 2 * row-bound form
+    for kind, src, Ls, extra in ((1, IMM_SOURCE, IMM_LS, ()), (2, IMM2_SOURCE, IMM2_LS, ()),
+                                  (3, IMM8_SOURCE, IMM8_LS, ()),
+                                  (4, IMM8_SOURCE, IMM8S_LS, ("-DQB_IMM8_SUPER=1",)),
+                                  (5, IMM8_SOURCE, IMM8_LS, ("-DQB_IMM8_APPROX=1",)),
+                                  (6, IMM8_SOURCE, IMM8S_LS, ("-DQB_IMM8_SUPER=1", "-DQB_IMM8_APPROX=1"))):
         for L in Ls:
             cub = os.path.join(objdir, f"qb_coarse_imm{kind}_L{L}.cubin")
             cmd = ["nvcc", *[f for f in compile_flags if not f.startswith("-Xcompiler") and "-fPIC" not in f],
-                   f"-DQB_IMM_L={L}", "-cubin", "-o", cub, src]
+                   f"-DQB_IMM_L={L}", *extra, "-cubin", "-o", cub, src]
             procs.append((f"{src} (L={L})", subprocess.Popen(cmd)))
             cubins.append((kind, L, cub))
     failed = [src for src, p in procs if p.wait() != 0]

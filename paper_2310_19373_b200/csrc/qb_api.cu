@@ -231,7 +231,8 @@ static int ensure_host(T** ptr, size_t* cap, size_t need) {
 extern "C" {
 struct qb_imm_cubin {
   int kind;  // 1: coarse_kernel<.., IMM = true> (10-bit pass), 2: coarse2_kernel (11-bit super-blocks),
-             // 3: coarse8_kernel (byte-packed threshold pass), 4: coarse8s_kernel (its super-block form)
+             // 3: coarse8_kernel (byte-packed threshold pass), 4: coarse8s_kernel (its super-block form),
+             // 5 / 6: the row-bound (APPROX) forms of 3 / 4
   int L;
   const unsigned char* data;
   size_t size;
@@ -244,6 +245,9 @@ constexpr int kImmWords = 1 << (BMAX - 1);  // Tc2 words = placeholders of the 1
 constexpr int kImm2Words = 1 << BMAX;       // Tc11 words = placeholders of the super-block kernel
 constexpr int kImm8Words = 1 << (BMAX - 2);  // byte-packed words = placeholders of the threshold kernel
 constexpr int kImm8sWords = 1 << (BMAX - 1);  // ... of its super-block form (11 image bits)
+static int imm_nwords_of(int kind) {
+  return kind == 1 ? kImmWords : kind == 2 ? kImm2Words : (kind == 4 || kind == 6) ? kImm8sWords : kImm8Words;
+}
 
 // Write words[idx] into every SASS instruction whose 32-bit immediate (bits 32..63 of the first
 // instruction word) is QB_IMM_PH | idx, in every .text section.  Each placeholder must occur exactly
@@ -290,15 +294,15 @@ static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words, in
   return kernels == 1;
 }
 
+// kinds 3..6 of the byte-packed threshold kernels: 3 + super + 2 * approx
+static bool imm8_super(int kind) { return kind == 4 || kind == 6; }
+static bool imm8_approx(int kind) { return kind == 5 || kind == 6; }
 static std::string imm_kernel_name(int kind, int L) {
-  if (kind == 4)
-    return "_ZN2qb15coarse8s_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
-           std::to_string(QB_COARSE_B1) + "ELi" + std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" +
-           std::to_string(TPB) + "EEEvNS_11TableParamsE";
-  if (kind == 3)
-    return "_ZN2qb14coarse8_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
-           std::to_string(QB_COARSE_B1) + "ELi" + std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" +
-           std::to_string(TPB) + "EEEvNS_11TableParamsE";
+  if (kind >= 3)  // 3..6: coarse8[s]_kernel<..., APPROX>
+    return std::string(imm8_super(kind) ? "_ZN2qb15coarse8s_kernelILi" : "_ZN2qb14coarse8_kernelILi") +
+           std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" + std::to_string(QB_COARSE_B1) + "ELi" +
+           std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" + std::to_string(TPB) + "ELb" +
+           (imm8_approx(kind) ? "1" : "0") + "EEEvNS_11TableParamsE";
   if (kind == 2)
     return "_ZN2qb14coarse2_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
            std::to_string(L) + "ELi" + std::to_string(TPB) + "EEEvNS_11TableParamsE";
@@ -376,7 +380,7 @@ static bool imm_enabled() {
 }
 
 #ifndef QB_IMM_AUTO_KIND
-#define QB_IMM_AUTO_KIND 1  // AUTO's patched-immediate kernel: 1 = 10-bit blocks (n=40: 29.6 ms), 2 = 11-bit super-blocks (30.3 ms)
+#define QB_IMM_AUTO_KIND 4  // AUTO's patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3 ms), 3 = byte-packed threshold pass (22.7 ms), 4 = its super-blocks (21.7 ms)
 #endif
 static int imm_auto_kind() {
   const char* e = std::getenv("QB_IMM_KIND");
@@ -582,14 +586,17 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
   P.c8_shift = 0;
   P.c8_rneg = 0;
   P.c8_pad = 0;
-  if (imm8_image && B == BMAX && (imm8_image == 1 || n > B)) {
+  if (imm8_image && B == BMAX && ((imm8_image & 3) == 1 || n > B)) {
     // byte image of the threshold kernels (qb_coarse8.cuh); imm8_image == 2: the super-block form, whose
     // image also covers bit B (NB = B + 1 image bits, fields formed from the bits above B only).
     // H_i = sum_{q >= NB} x_q q_iq lies in [hneg_i, hpos_i] for every state, rint is monotone and the device
     // forms H_i 2^-s exactly, so hc_i lies in [rint(hneg_i 2^-s), rint(hpos_i 2^-s)].
     // X(z) = sum_{i in z} hc_i + Tc8(z) is bounded over the 2^NB image states by doubling; s8 is the smallest
     // shift with Rneg + Rpos <= 127.
-    const int NB = imm8_image == 2 ? B + 1 : B;
+    const int NB = (imm8_image & 3) == 2 ? B + 1 : B;
+    // row-bound form (imm8_image & 4): the row bits (QB_COARSE_B2 .. NB-1) enter every byte as the constant
+    // amin = sum min(hc_i, 0) instead of their subset sums
+    const bool approx8 = (imm8_image & 4) != 0;
     double hpos[BMAX + 1], hneg[BMAX + 1];
     for (int i = 0; i < NB; ++i) {
       hpos[i] = hneg[i] = 0.0;
@@ -615,21 +622,26 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
     for (int s8 = 0; s8 <= 60; ++s8) {
       const double sc8 = std::ldexp(1.0, -s8);
       up[0] = dn[0] = 0;
+      int row_floor = 0;  // row-bound form: the least value amin can take (<= 0)
       for (int i = 0; i < NB; ++i) {
-        const int cp = (int)std::nearbyint(hpos[i] * sc8), cn = (int)std::nearbyint(hneg[i] * sc8);
+        int cp = (int)std::nearbyint(hpos[i] * sc8), cn = (int)std::nearbyint(hneg[i] * sc8);
+        if (approx8 && i >= QB_COARSE_B2) {
+          row_floor += std::min(cn, 0);
+          cp = cn = 0;
+        }
         for (int z = 0; z < (1 << i); ++z) {
           up[z + (1 << i)] = up[z] + cp;
           dn[z + (1 << i)] = dn[z] + cn;
         }
       }
       bool fits = true;
-      int rpos = 0, rneg = 0;
+      int rpos = 0, rneg = -row_floor;
       for (int z = 0; z < (1 << NB); ++z) {
         const double t = std::nearbyint(timg[z] * sc8);
         if (std::fabs(t) > 127.0) { fits = false; break; }
         tc8[z] = (int)t;
         rpos = std::max(rpos, up[z] + tc8[z]);
-        rneg = std::max(rneg, -(dn[z] + tc8[z]));
+        rneg = std::max(rneg, -(dn[z] + tc8[z]) - row_floor);
       }
       if (!fits || rpos + rneg > 127) continue;
       P.c8_shift = s8;
@@ -825,7 +837,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8S) return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8AS) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -854,38 +866,39 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const bool tc = want_tc && pl.ks->tc != nullptr;
   const bool coarse = !tc && pl.ks->coarse != nullptr &&
                       (variant == QB_VARIANT_COARSE || variant == QB_VARIANT_TC || variant == QB_VARIANT_IMM ||
-                       variant == QB_VARIANT_IMM2 || variant == QB_VARIANT_IMM8 || variant == QB_VARIANT_IMM8S ||
-                       (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
+                       variant >= QB_VARIANT_IMM2 || (variant == QB_VARIANT_AUTO && blocks_per_thread >= 32.0));
   // the coarse pass with the instance's table as instruction immediates (AUTO: whenever the coarse kernel
   // runs, unless QB_IMM=0); QB_VARIANT_COARSE forces the table-load coarse kernel.  Kind 2 = the 11-bit
   // super-block kernel (needs L >= B + 2), AUTO's kind unless QB_IMM_KIND=1.
-  bool imm = coarse && (variant == QB_VARIANT_IMM || variant == QB_VARIANT_IMM2 || variant == QB_VARIANT_IMM8 ||
-                        variant == QB_VARIANT_IMM8S ||
-                        (variant == QB_VARIANT_AUTO && imm_enabled()));
+  bool imm = coarse && (variant >= QB_VARIANT_IMM || (variant == QB_VARIANT_AUTO && imm_enabled()));
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit kernel, reported as IMM)
   int imm_kind = !imm                                ? 0
                  : variant == QB_VARIANT_IMM         ? 1
                  : variant == QB_VARIANT_IMM8        ? 3
                  : variant == QB_VARIANT_IMM8S       ? 4
+                 : variant == QB_VARIANT_IMM8A       ? 5
+                 : variant == QB_VARIANT_IMM8AS      ? 6
                  : variant == QB_VARIANT_AUTO        ? imm_auto_kind()
                                                      : 2;
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit form of the same pass)
   if (imm_kind == 2 && L < BMAX + 2) imm_kind = 1;
-  if (imm_kind == 4 && L < BMAX + 2) imm_kind = 3;
+  if (imm8_super(imm_kind) && L < BMAX + 2) imm_kind -= 1;
   QB_TMARK("geometry");
   // the host seed must be a value some searched state attains: whole-space searches (m_fix == 0) of the
   // coarse and tensor-core kernels, any chunk length; shards use it too (the combine treats a shard
   // that finds nothing <= the seed as empty, see the shard handling below)
   const bool seed = (coarse || tc) && m_fix == 0 && n >= 24;
-  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2, imm_kind == 4 ? 2 : imm_kind == 3 ? 1 : 0)) return rc;
+  if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2,
+                        imm_kind < 3 ? 0 : (imm8_super(imm_kind) ? 2 : 1) | (imm8_approx(imm_kind) ? 4 : 0)))
+    return rc;
   QB_TMARK("quantize");
-  if (imm_kind >= 3 && pl.imm8_words.size() != (size_t)(imm_kind == 4 ? kImm8sWords : kImm8Words)) {
+  if (imm_kind >= 3 && pl.imm8_words.size() != (size_t)imm_nwords_of(imm_kind)) {
     // no shift makes the block's coarse range fit a byte (cannot happen for finite coefficients, kept as a guard)
     if (variant != QB_VARIANT_AUTO) return fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
     imm_kind = 1;
   }
   const unsigned* imm_words = imm_kind >= 3 ? pl.imm8_words.data() : imm_kind == 2 ? pl.imm2_words.data() : pl.P->Tc2;
-  const int imm_nwords = imm_kind == 4 ? kImm8sWords : imm_kind == 3 ? kImm8Words : imm_kind == 2 ? kImm2Words : kImmWords;
+  const int imm_nwords = imm_nwords_of(imm_kind);
   if (imm_kind == 2 && pl.imm2_words.size() != (size_t)kImm2Words) return fail(QB_E_INTERNAL, "no 11-bit coarse image");
 
   TableParams& P = *pl.P;
@@ -924,7 +937,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->module_ms = module_ms;
   out->variant = fieldwalk ? QB_VARIANT_FIELDWALK
                  : tc      ? QB_VARIANT_TC
-                 : imm     ? (imm_kind == 4   ? QB_VARIANT_IMM8S
+                 : imm     ? (imm_kind == 6   ? QB_VARIANT_IMM8AS
+                              : imm_kind == 5 ? QB_VARIANT_IMM8A
+                              : imm_kind == 4 ? QB_VARIANT_IMM8S
                               : imm_kind == 3 ? QB_VARIANT_IMM8
                               : imm_kind == 2 ? QB_VARIANT_IMM2
                                               : QB_VARIANT_IMM)
@@ -1676,14 +1691,13 @@ int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const in
 
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size) {
   if (!words || !size) return qb::fail(QB_E_ARG, "null pointer");
-  if (kind < 1 || kind > 4)
-    return qb::fail(QB_E_ARG, "kind must be 1 (10-bit), 2 (super-block), 3 (byte-packed) or 4 (byte-packed super-block)");
+  if (kind < 1 || kind > 6) return qb::fail(QB_E_ARG, "kind must be 1..6 (see qubrute_b200.h)");
   const qb_imm_cubin* cb = nullptr;
   for (const qb_imm_cubin* c = qb_imm_cubins; c->data; ++c)
     if (c->L == L && c->kind == kind) cb = c;
   if (!cb) return qb::fail(QB_E_ARG, "no patched-immediate cubin for L=" + std::to_string(L));
   std::vector<unsigned char> img(cb->data, cb->data + cb->size);
-  if (!qb::imm_patch(img, words, kind == 4 ? qb::kImm8sWords : kind == 3 ? qb::kImm8Words : kind == 2 ? qb::kImm2Words : qb::kImmWords))
+  if (!qb::imm_patch(img, words, qb::imm_nwords_of(kind)))
     return qb::fail(QB_E_INTERNAL, "patched-immediate cubin rejected (placeholders)");
   *size = img.size();
   if (out && cap >= img.size()) std::memcpy(out, img.data(), img.size());

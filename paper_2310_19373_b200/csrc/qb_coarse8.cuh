@@ -43,6 +43,9 @@
 #ifndef QB_IMM8_LAZY
 #define QB_IMM8_LAZY 9  // of the 16 registers of a row, those whose A_u + table add is one IADD3 (ALU pipe); measured n=40: 8: 25.4, 9: 22.7, 10: 23.2, 11: 23.1, 12: 24.2 ms
 #endif
+#ifndef QB_IMM8A_ALU
+#define QB_IMM8A_ALU 4  // row-bound form: of the 16 adds of a row, those issued as IADD3 on the ALU pipe (the rest: IMAD)
+#endif
 #ifndef QB_IMM8_MINB
 #define QB_IMM8_MINB 4
 #endif
@@ -59,7 +62,15 @@ __device__ __forceinline__ unsigned add_fma_reg(unsigned a, unsigned one, unsign
 // AND of the bytes f(z) of a block (four per register); see the file header.  SUPER: the rows also run
 // over one more bit (the first outer bit, field hcx = rint(F_B 2^-s8)): 32 rows, the first 16 of the Gray
 // walk are the block with that bit 0 (out[0]), the last 16 the block with it 1 (out[1]).
-template <int CB1, int CB2, bool SUPER>
+//
+// APPROX (QB_VARIANT_IMM8A / IMM8AS, the "row-bound" form): every row uses the SAME row term, the least one,
+// amin = sum_{i in u bits} min(hc_i, 0) <= A_u, folded into the base.  A state's byte is then a lower bound
+// of its coarse value (low by A_u - amin >= 0), so the test stays certified -- a block with no byte under the
+// limit still holds no state under it -- but passes more blocks to the exact evaluation.  In exchange a row
+// costs one 2-input add per register (either integer pipe) instead of a 3-input IADD3 or two IMADs, and
+// the per-row A_u chain disappears.  Pays when the row fields are small against the spread of block
+// minima (sparse instances such as config E); AUTO decides from the instance (qb_api.cu).
+template <int CB1, int CB2, bool SUPER, bool APPROX = false>
 __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2], float FB, int base,
                                                   unsigned (&out)[2]) {
   constexpr int B = CB1 + CB2, UB = CB1 + (SUPER ? 1 : 0), NU = 1 << UB, NQ = 1 << (CB2 - 2);
@@ -67,6 +78,43 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
   int hc[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) hc[i] = __float2int_rn(H[i] * p.c8_scale);
+  const unsigned one = p.imm_one;
+  if constexpr (APPROX) {
+    int amin = 0;
+#pragma unroll
+    for (int i = 0; i < CB1; ++i) amin += min(hc[CB2 + i], 0);
+    if constexpr (SUPER) amin += min(__float2int_rn(FB * p.c8_scale), 0);
+    // 0, opaque to ptxas and re-derived per row (else the compiler hoists X4[q] + zero out of the row loop and
+    // issues 2-input VIADDs, which run on the FMA-heavy pipe): makes the ALU-pipe adds 3-input IADD3s
+    const unsigned zero = (unsigned)p.c8_pad;
+    // X4[q] byte j = base + amin + sum_{i in w} hc_i, w = 4q + j
+    unsigned X4[NQ];
+    X4[0] = (unsigned)(base + amin) * 0x01010101u + (unsigned)hc[0] * 0x01000100u + (unsigned)hc[1] * 0x01010000u;
+#pragma unroll
+    for (int i = 2; i < CB2; ++i) {
+      const unsigned d = (unsigned)hc[i] * 0x01010101u;
+#pragma unroll
+      for (int m = 0; m < (1 << (i - 2)); ++m) X4[m + (1 << (i - 2))] = X4[m] + d;
+    }
+    unsigned acc[2][2] = {{0xffffffffu, 0xffffffffu}, {0xffffffffu, 0xffffffffu}};
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int half = SUPER ? (u >> CB1) : 0;
+      const unsigned ph = QB_IMM_PH | (unsigned)(u * NQ);
+      const unsigned zrow = zero & (0x9E3779B9u * (unsigned)(u + 1));  // 0, a different expression per row
+      unsigned r[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const bool alu = ((q + 1) * QB_IMM8A_ALU) / NQ > (q * QB_IMM8A_ALU) / NQ;
+        r[q] = alu ? X4[q] + zrow + (ph | (unsigned)q) : add_fma_pipe(X4[q], one, ph | q);
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; q += 2) acc[half][(q >> 1) & 1] &= r[q] & r[q + 1];
+    }
+    out[0] = acc[0][0] & acc[0][1];
+    out[1] = acc[1][0] & acc[1][1];
+    return;
+  }
   // X4[q] byte j = base + sum_{i in w} hc_i, w = 4q + j
   unsigned X4[NQ];
   X4[0] = (unsigned)base * 0x01010101u + (unsigned)hc[0] * 0x01000100u + (unsigned)hc[1] * 0x01010000u;
@@ -80,7 +128,6 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
 #pragma unroll
   for (int i = 0; i < CB1; ++i) du[i] = (unsigned)hc[CB2 + i] * 0x01010101u;
   if constexpr (SUPER) du[CB1] = (unsigned)__float2int_rn(FB * p.c8_scale) * 0x01010101u;
-  const unsigned one = p.imm_one;
   unsigned a4 = 0u;
   unsigned acc[2][2] = {{0xffffffffu, 0xffffffffu}, {0xffffffffu, 0xffffffffu}};
 #pragma unroll
@@ -107,7 +154,7 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
   out[1] = acc[1][0] & acc[1][1];
 }
 
-template <int B1, int B2, int CB1, int CB2, int L, int TPB>
+template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false>
 __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(CB1 + CB2 == B, "coarse split must cover the table bits");
@@ -155,7 +202,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
       const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
       const int lc = (int)min(max(lrel, lc_min), -1ll);
       unsigned a[2];
-      coarse8_block_and<CB1, CB2, false>(p, H, 0.f, 127 - lc, a);
+      coarse8_block_and<CB1, CB2, false, APPROX>(p, H, 0.f, 127 - lc, a);
       if (lrel < 0 && (a[0] & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
       const long long val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
       cmin = min(cmin, val);
@@ -181,7 +228,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
 // B+1 .. L-1, and each half that holds a byte under the limit is re-evaluated exactly from its own base,
 // in original block order j = 2 j' + (b ^ (j' & 1)), so keys, records and finalize_kernel see the
 // blocks of the 10-bit walk.  Certified bound: (11 + 1)/2 coarse units.
-template <int B1, int B2, int CB1, int CB2, int L, int TPB>
+template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false>
 __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(CB1 + CB2 == B && B == BMAX, "super-blocks extend the 10-bit table blocks");
@@ -229,7 +276,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
       const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
       const int lc = (int)min(max(lrel, lc_min), -1ll);
       unsigned a[2];
-      coarse8_block_and<CB1, CB2, true>(p, H, F[0], 127 - lc, a);
+      coarse8_block_and<CB1, CB2, true, APPROX>(p, H, F[0], 127 - lc, a);
       if (lrel < 0 && (a[0] & a[1] & 0x80808080u) == 0x80808080u) continue;  // neither half holds a state under the limit
 #pragma unroll 1
       for (int t = 0; t < 2; ++t) {

@@ -1,6 +1,8 @@
-// Byte-packed threshold search kernels (QB_VARIANT_IMM8, qb_coarse8.cuh), compiled to one standalone
-// cubin per chunk length (-DQB_IMM_L=<L>) and embedded in libqubrute_b200.so like the 16-bit ones
-// (qb_k_coarse_imm.cu).  Kernel names: qb::coarse8_kernel<BIG_B1, BIG_B2, QB_COARSE_B1, QB_COARSE_B2, L, TPB>.
+// Byte-packed threshold search kernels (qb_coarse8.cuh), compiled to one standalone cubin per chunk
+// length (-DQB_IMM_L=<L>) and form (-DQB_IMM8_SUPER=0/1: 10-bit blocks or 11-bit super-blocks;
+// -DQB_IMM8_APPROX=0/1: exact row terms or the row-bound form), embedded in libqubrute_b200.so like the
+// 16-bit ones (qb_k_coarse_imm.cu).  Kernel names:
+// qb::coarse8[s]_kernel<BIG_B1, BIG_B2, QB_COARSE_B1, QB_COARSE_B2, L, TPB, APPROX>.
 #include "qb_coarse8.cuh"
 #include "qb_registry.h"
 
@@ -9,7 +11,18 @@ namespace qb {
 #ifndef QB_IMM_L
 #error "build with -DQB_IMM_L=<chunk length>"
 #endif
-template __global__ void coarse8_kernel<BIG_B1, BIG_B2, QB_COARSE_B1, QB_COARSE_B2, QB_IMM_L, TPB>(
+#ifndef QB_IMM8_SUPER
+#define QB_IMM8_SUPER 0
+#endif
+#ifndef QB_IMM8_APPROX
+#define QB_IMM8_APPROX 0
+#endif
+#if QB_IMM8_SUPER
+template __global__ void coarse8s_kernel<BIG_B1, BIG_B2, QB_COARSE_B1, QB_COARSE_B2, QB_IMM_L, TPB, QB_IMM8_APPROX != 0>(
     const __grid_constant__ TableParams);
+#else
+template __global__ void coarse8_kernel<BIG_B1, BIG_B2, QB_COARSE_B1, QB_COARSE_B2, QB_IMM_L, TPB, QB_IMM8_APPROX != 0>(
+    const __grid_constant__ TableParams);
+#endif
 
 }  // namespace qb

@@ -23,7 +23,7 @@ CASES = [("E", 40, 0), ("E", 40, 1), ("E", 36, 2), ("E", 33, 3), ("D", 32, 0), (
          ("B", 34, 2), ("A", 32, 5)]
 
 
-IMMS = [_lib.VARIANT_IMM, _lib.VARIANT_IMM2, _lib.VARIANT_IMM8, _lib.VARIANT_IMM8S]
+IMMS = [_lib.VARIANT_IMM, _lib.VARIANT_IMM2, _lib.VARIANT_IMM8, _lib.VARIANT_IMM8S, _lib.VARIANT_IMM8A, _lib.VARIANT_IMM8AS]
 
 
 @pytest.mark.parametrize("var", IMMS)

@@ -13,7 +13,7 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 for n in ns:
     c = instances.config_coeffs(name, 0, n=n)
     out = {}
-    for var, label in ((_lib.VARIANT_IMM, "imm"), (_lib.VARIANT_IMM8, "imm8"), (_lib.VARIANT_IMM8S, "imm8s")):
+    for var, label in ((_lib.VARIANT_IMM, "imm"), (_lib.VARIANT_IMM8, "imm8"), (_lib.VARIANT_IMM8S, "imm8s"), (_lib.VARIANT_IMM8A, "imm8a"), (_lib.VARIANT_IMM8AS, "imm8as")):
         _lib.solve(c, variant=var)
         rs = [_lib.solve(c, variant=var) for _ in range(reps)]
         r = rs[-1]
@@ -21,4 +21,4 @@ for n in ns:
         print(f"{name} n={n} {label:5s} search {statistics.median(x.search_ms for x in rs):.3f} ms  kernel "
               f"{statistics.median(x.kernel_ms for x in rs):.3f} ms  total {statistics.median(x.total_ms for x in rs):.3f} ms  "
               f"argmin {hex(r.argmin_bits)} value {r.value!r} cand {r.candidates} variant {r.variant}", flush=True)
-    print("MATCH" if out["imm"] == out["imm8"] == out["imm8s"] else f"MISMATCH {out}", flush=True)
+    print("MATCH" if all(v == out["imm"] for v in out.values()) else f"MISMATCH {out}", flush=True)
