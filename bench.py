@@ -96,16 +96,13 @@ def imm_sass_sha256(L: int, kind: int = 1):
     from paper_2310_19373_b200 import _lib
 
     try:
-        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(IMM_WORDS[kind], dtype=np.uint32), kind)
+        img = _lib.imm_image(L, np.uint32(0x7A5C0000) | np.arange(_lib.IMM_WORDS[kind], dtype=np.uint32), kind)
     except Exception:  # noqa: BLE001 - no cubin for this L / library without the IMM kernels
         return None
     with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
         fh.write(img)
         fh.flush()
         return sass_sha256(fh.name, imm_symbol(L, kind))
-
-
-IMM_WORDS = {1: 512, 2: 1024, 3: 256, 4: 512, 5: 256, 6: 512}  # placeholder immediates per patched kernel kind
 
 
 def imm_symbol(L: int, kind: int = 1) -> str:

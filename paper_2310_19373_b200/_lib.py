@@ -30,6 +30,7 @@ IMM2_LS = (12, 13, 14, 16, 18, 20, 22)  # super-block kernel: chunks of >= B + 2
 IMM8_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse8_imm.cu")  # byte-packed threshold kernel
 IMM8_LS = IMM_LS
 IMM8S_LS = IMM2_LS  # its 11-bit super-block form
+IMM_WORDS = {1: 512, 2: 1024, 3: 256, 4: 512, 5: 256, 6: 512}  # placeholder immediates per patched kernel kind
 
 QB_OK = 0
 QB_E_ARG = -1
@@ -352,11 +353,11 @@ def prefix_eval(coeffs, k: int, c_begin: int, count: int, device: int | None = N
 
 
 def imm_image(L: int, words, kind: int = 1) -> bytes:
-    """The patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 512 words; 2: QB_VARIANT_IMM2, 1024
-    words) for chunk length L with coarse table words `words` (test hook)."""
+    """The patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 2: IMM2, 3: IMM8, 4: IMM8S, 5: IMM8A,
+    6: IMM8AS; IMM_WORDS[kind] table words) for chunk length L with coarse table words `words` (test hook)."""
     w = np.ascontiguousarray(words, dtype=np.uint32)
-    if w.shape != ((512,) if kind == 1 else (1024,)):
-        raise ValueError("need 512 (kind 1) or 1024 (kind 2) table words")
+    if kind not in IMM_WORDS or w.shape != (IMM_WORDS[kind],):
+        raise ValueError(f"kind {kind} needs {IMM_WORDS.get(kind)} table words")
     size = ctypes.c_uint64()
     wp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
     check(lib().qb_imm_image(kind, L, wp, None, 0, ctypes.byref(size)), "qb_imm_image")
