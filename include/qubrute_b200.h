@@ -163,6 +163,14 @@ int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_
  * *size receives the image size; the image is copied to `out` when cap >= *size. */
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);
 
+/* Test hook (host only): the byte image the threshold kernels (kind 3..6 = QB_VARIANT_IMM8, IMM8S, IMM8A, IMM8AS)
+ * would run `coeffs` with: the packed table words (256 for kinds 3 / 5, 512 for 4 / 6), the quantized upper-
+ * triangular instance (n * n doubles, integer-valued, coefficient * 2^scale_exp rounded), fl(1 / unit), the range
+ * bound Rneg and the certified rounding margin (quantized units).  tests/test_byte_image_cpu.py replays the
+ * device's block test on it and checks the range and no-false-negative claims of qb_coarse8.cuh. */
+int qb_byte_image(const double* coeffs, int n, int kind, uint32_t* words, double* quantized, float* inv_unit,
+                  int32_t* rneg, int64_t* slack, int32_t* scale_exp);
+
 #ifdef __cplusplus
 }
 #endif

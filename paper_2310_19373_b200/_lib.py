@@ -120,6 +120,9 @@ SIGNATURES = {
     "qb_prefix_eval": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _dp, _dp]),
     "qb_imm_image": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), ctypes.c_char_p,
                                     ctypes.c_uint64, _u64p]),
+    "qb_byte_image": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), _dp,
+                                     ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]),
 }
 
 _lock = threading.Lock()
@@ -350,6 +353,20 @@ def prefix_eval(coeffs, k: int, c_begin: int, count: int, device: int | None = N
     rc = lib().qb_prefix_eval(_ptr(c), n, k, c_begin, count, _ptr(vals), _ptr(fields))
     check(rc, "qb_prefix_eval")
     return vals, fields
+
+
+def byte_image(coeffs, kind: int):
+    """Host-only test hook: (words, quantized upper-triangular Q, fl(1/unit), Rneg, slack, scale_exp) of the byte
+    image the threshold kernel of `kind` (3..6) builds for `coeffs` (qb_byte_image)."""
+    c = _f64(coeffs)
+    n = c.shape[0]
+    words = np.zeros(IMM_WORDS[kind], dtype=np.uint32)
+    quant = np.zeros((n, n), dtype=np.float64)
+    inv, rneg, slack, e = ctypes.c_float(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()
+    check(lib().qb_byte_image(_ptr(c), n, kind, words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), _ptr(quant),
+                              ctypes.byref(inv), ctypes.byref(rneg), ctypes.byref(slack), ctypes.byref(e)),
+          "qb_byte_image")
+    return words, quant, np.float32(inv.value), int(rneg.value), int(slack.value), int(e.value)
 
 
 def imm_image(L: int, words, kind: int = 1) -> bytes:

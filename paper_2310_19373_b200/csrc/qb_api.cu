@@ -584,16 +584,18 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
     P.coarse_scale = (float)sc11;
   }
   P.c8_scale = 1.f;
-  P.c8_shift = 0;
   P.c8_rneg = 0;
+  P.c8_zero = 0;
   P.c8_pad = 0;
+  P.c8_slack = 0;
   if (imm8_image && B == BMAX && ((imm8_image & 3) == 1 || n > B)) {
-    // byte image of the threshold kernels (qb_coarse8.cuh); imm8_image == 2: the super-block form, whose
+    // byte image of the threshold kernels (qb_coarse8.cuh); (imm8_image & 3) == 2: the super-block form, whose
     // image also covers bit B (NB = B + 1 image bits, fields formed from the bits above B only).
-    // H_i = sum_{q >= NB} x_q q_iq lies in [hneg_i, hpos_i] for every state, rint is monotone and the device
-    // forms H_i 2^-s exactly, so hc_i lies in [rint(hneg_i 2^-s), rint(hpos_i 2^-s)].
-    // X(z) = sum_{i in z} hc_i + Tc8(z) is bounded over the 2^NB image states by doubling; s8 is the smallest
-    // shift with Rneg + Rpos <= 127.
+    // H_i = sum_{q >= NB} x_q q_iq lies in [hneg_i, hpos_i] for every state; the device forms
+    // hc_i = rint(fl(H_i * fl(1/U))) and both roundings are monotone, so hc_i lies in [hcn_i, hcp_i], the same
+    // expression at hneg_i and hpos_i (computed here in float exactly as on the device).
+    // X(z) = sum_{i in z} hc_i + Tc8(z) is bounded over the 2^NB image states by doubling; the unit U is the
+    // smallest of a few candidates with Rneg + Rpos <= 127.
     const int NB = (imm8_image & 3) == 2 ? B + 1 : B;
     // row-bound form (imm8_image & 4): the row bits (QB_COARSE_B2 .. NB-1) enter every byte as the constant
     // amin = sum min(hc_i, 0) instead of their subset sums
@@ -619,13 +621,21 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
       const double qBB = q[(size_t)B * n + B];
       for (int z = 0; z < (1 << B); ++z) timg[(size_t)z + (1 << B)] = (double)P.T[z] + qBB + RB[z];
     }
+    double tmin = 0.0, tmax = 0.0, range = 0.0;
+    for (int z = 0; z < (1 << NB); ++z) {
+      tmin = std::min(tmin, timg[z]);
+      tmax = std::max(tmax, timg[z]);
+    }
+    for (int i = 0; i < NB; ++i) range += (approx8 && i >= QB_COARSE_B2) ? -hneg[i] : hpos[i] - hneg[i];
+    range += tmax - tmin;
     std::vector<int> tc8((size_t)1 << NB), up((size_t)1 << NB), dn((size_t)1 << NB);
-    for (int s8 = 0; s8 <= 60; ++s8) {
-      const double sc8 = std::ldexp(1.0, -s8);
+    // Rneg of unit U, or -1 when the image does not fit a byte
+    auto try_unit = [&](double U) -> int {
+      const float inv = (float)(1.0 / U);
       up[0] = dn[0] = 0;
       int row_floor = 0;  // row-bound form: the least value amin can take (<= 0)
       for (int i = 0; i < NB; ++i) {
-        int cp = (int)std::nearbyint(hpos[i] * sc8), cn = (int)std::nearbyint(hneg[i] * sc8);
+        int cp = (int)std::nearbyintf((float)hpos[i] * inv), cn = (int)std::nearbyintf((float)hneg[i] * inv);
         if (approx8 && i >= QB_COARSE_B2) {
           row_floor += std::min(cn, 0);
           cp = cn = 0;
@@ -635,24 +645,35 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
           dn[z + (1 << i)] = dn[z] + cn;
         }
       }
-      bool fits = true;
       int rpos = 0, rneg = -row_floor;
       for (int z = 0; z < (1 << NB); ++z) {
-        const double t = std::nearbyint(timg[z] * sc8);
-        if (std::fabs(t) > 127.0) { fits = false; break; }
+        const double t = std::nearbyint(timg[z] / U);
+        if (std::fabs(t) > 127.0) return -1;
         tc8[z] = (int)t;
         rpos = std::max(rpos, up[z] + tc8[z]);
         rneg = std::max(rneg, -(dn[z] + tc8[z]) - row_floor);
       }
-      if (!fits || rpos + rneg > 127) continue;
-      P.c8_shift = s8;
-      P.c8_scale = (float)sc8;
+      return rpos + rneg <= 127 ? rneg : -1;
+    };
+    // each rounded field and table entry is within 1/2 of its real value, so the real range / U plus
+    // (NB + 1) / 2 on each side bounds Rneg + Rpos: this first unit always fits; then two finer ones are tried
+    double U = std::max(1.0, range / (127.0 - (NB + 2)));
+    int rneg = try_unit(U);
+    for (int guard = 0; rneg < 0 && guard < 64; ++guard) rneg = try_unit(U *= 1.0625);
+    if (rneg >= 0) {
+      for (double f : {0.9, 0.95}) {
+        const double U2 = std::max(1.0, U * f);
+        const int r2 = U2 < U ? try_unit(U2) : -1;
+        if (r2 >= 0) { U = U2; rneg = r2; break; }
+      }
+      rneg = try_unit(U);  // leaves tc8 of the chosen unit
+      P.c8_scale = (float)(1.0 / U);
       P.c8_rneg = rneg;
+      P.c8_slack = (long long)std::ceil(U * (0.5 * (NB + 1) + 0.02));
       // word z >> 2 = u * 16 + q: bytes j = 0..3 hold Tc8(z), z = (u << 6) | (4 q + j); signed bytes summed mod 2^32
       pl.imm8_words.assign((size_t)1 << (NB - 2), 0u);
       for (int z = 0; z < (1 << NB); ++z)
         pl.imm8_words[z >> 2] += (unsigned)tc8[z] << (8 * (z & 3));
-      break;
     }
   }
   // coarse image for the tensor-core pass (qb_tc.cuh): D(z) = sum_i z_i hc_i + Tc(z) + beta must lie
@@ -1687,6 +1708,30 @@ int qb_solve_batch_devices(const double* coeffs, int n, uint64_t count, const in
       return qb::fail(rcs[i], "slice " + std::to_string(i) + " (instances from " + std::to_string(b0) + "): " + errs[i]);
     }
   if (kernel_ms) *kernel_ms = *std::max_element(ms.begin(), ms.end());
+  return QB_OK;
+}
+
+int qb_byte_image(const double* coeffs, int n, int kind, uint32_t* words, double* quantized, float* inv_unit,
+                  int32_t* rneg, int64_t* slack, int32_t* scale_exp) {
+  if (!coeffs || !words || !quantized || !inv_unit || !rneg || !slack || !scale_exp)
+    return qb::fail(QB_E_ARG, "null pointer");
+  if (kind < 3 || kind > 6) return qb::fail(QB_E_ARG, "kind must be 3..6 (byte-packed threshold kernels)");
+  if (n <= qb::BMAX || n > QB_MAX_DIM) return qb::fail(QB_E_ARG, "needs BMAX < n <= QB_MAX_DIM");
+  qb::Plan pl;
+  pl.n = n;
+  pl.P = std::make_unique<qb::TableParams>();
+  const int img = (qb::imm8_super(kind) ? 2 : 1) | (qb::imm8_approx(kind) ? 4 : 0);
+  if (int rc = qb::quantize(coeffs, n, qb::BMAX, qb::BMAX, pl, false, false, false, img)) return rc;
+  if (pl.imm8_words.size() != (size_t)qb::imm_nwords_of(kind))
+    return qb::fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
+  std::memcpy(words, pl.imm8_words.data(), pl.imm8_words.size() * sizeof(uint32_t));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      quantized[(size_t)i * n + j] = i == j ? (double)pl.P->d[i] : (j > i ? (double)pl.P->Qs[i][j] : 0.0);
+  *inv_unit = pl.P->c8_scale;
+  *rneg = pl.P->c8_rneg;
+  *slack = pl.P->c8_slack;
+  *scale_exp = pl.e;
   return QB_OK;
 }
 

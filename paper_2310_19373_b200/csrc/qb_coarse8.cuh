@@ -9,15 +9,15 @@
 //
 //     f(z) = base + sum_{i in z} hc_i + Tc8(z),     base = 127 - Lc
 //
-// where hc_i = rint(H_i 2^-s8), Tc8(z) = rint(T(z) 2^-s8) (coarse unit 2^s8 quantized units) and Lc is the
-// block's own limit in coarse units, Lc = floor((lim - V) / 2^s8): bit 7 of f(z) is CLEAR exactly when the
+// where hc_i = rint(H_i / U), Tc8(z) = rint(T(z) / U) (coarse unit U quantized units, any real U >= 1) and Lc is
+// the block's own limit in coarse units, Lc = floor((lim - V) / U): bit 7 of f(z) is CLEAR exactly when the
 // state's coarse value is <= the limit.  Four states share a register (w = 4q .. 4q+3), the adds are
 // plain 32-bit adds, and one LOP3 ANDs two result registers into an accumulator: the block holds a
 // state under the limit iff some byte of the AND has bit 7 clear.  Every state's coarse value is
 // still formed and tested -- one add per four states plus half a LOP3, against one add per two states
 // plus a packed min in the 16-bit pass.
 //
-// Range (host, quantize(): c8_rneg / the choice of s8): with X(z) = sum hc_i z_i + Tc8(z) in [-Rneg, Rpos]
+// Range (host, quantize(): c8_rneg / the choice of U): with X(z) = sum hc_i z_i + Tc8(z) in [-Rneg, Rpos]
 // over every state and every reachable field vector, and Rneg + Rpos <= 127, the limit is clamped to
 // Lc in [-Rneg - 1, -1].  Lc >= 0 means z = 0 (coarse value 0) is under the limit: the block is
 // re-evaluated without looking at the bytes.  Lc < -Rneg - 1 means no state can be under it, and the
@@ -25,7 +25,8 @@
 // [128 - Rneg, 128 + Rneg + Rpos] = [1, 255]: no byte ever wraps or carries into its neighbour, and adding
 // a replicated or packed signed constant modulo 2^32 adds it to every byte exactly.
 //
-// Certified bound: as in the 16-bit pass, exact(z) >= V + (C(z) - (B+1)/2) 2^s8, and lim = thr + slack
+// Certified bound: as in the 16-bit pass, exact(z) >= V + (C(z) - (B+1)/2 - 0.02) U (the 0.02 covers the float
+// rounding of H_i fl(1/U)), and lim = thr + slack
 // (+ 2 Eq on the recording search, see below), so a block with no byte under the limit holds neither a
 // better state nor a tie.  Rows u (4 bits) run in reflected Gray order; a row's A_u (replicated in the
 // four bytes) is either added by a 3-input IADD3 together with the table immediate (ALU pipe) or by two
@@ -59,6 +60,14 @@ __device__ __forceinline__ unsigned add_fma_reg(unsigned a, unsigned one, unsign
   return r;
 }
 
+// A block's limit in coarse units: an integer >= floor(d / U) for d = lim - V (quantized units), from
+// the float product d * fl(1/U).  Its relative error is below 2^-22, i.e. below 2^-10 units wherever the
+// limit matters (|d / U| < 2^12; beyond that the limit is clamped or the block passes outright), so adding
+// 2^-10 before the floor never under-estimates it; over-estimating only passes more blocks.
+__device__ __forceinline__ int coarse8_limit(long long d, float inv_unit) {
+  return __float2int_rd(fmaf((float)d, inv_unit, 0.0009765625f));
+}
+
 // AND of the bytes f(z) of a block (four per register); see the file header.  SUPER: the rows also run
 // over one more bit (the first outer bit, field hcx = rint(F_B 2^-s8)): 32 rows, the first 16 of the Gray
 // walk are the block with that bit 0 (out[0]), the last 16 the block with it 1 (out[1]).
@@ -86,7 +95,7 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
     if constexpr (SUPER) amin += min(__float2int_rn(FB * p.c8_scale), 0);
     // 0, opaque to ptxas and re-derived per row (else the compiler hoists X4[q] + zero out of the row loop and
     // issues 2-input VIADDs, which run on the FMA-heavy pipe): makes the ALU-pipe adds 3-input IADD3s
-    const unsigned zero = (unsigned)p.c8_pad;
+    const unsigned zero = (unsigned)p.c8_zero;
     // X4[q] byte j = base + amin + sum_{i in w} hc_i, w = 4q + j
     unsigned X4[NQ];
     X4[0] = (unsigned)(base + amin) * 0x01010101u + (unsigned)hc[0] * 0x01000100u + (unsigned)hc[1] * 0x01010000u;
@@ -163,10 +172,10 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
   const int lane = threadIdx.x & 31;
-  // (B+1)/2 coarse units, quantized; the recording search adds the collect margin (file header)
-  const long long slack = ((long long)(B + 1) << p.c8_shift >> 1) + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);
-  const int sh = p.c8_shift;
-  const long long lc_min = -(long long)p.c8_rneg - 1;
+  // (B+1)/2 coarse units (+ float rounding), quantized; the recording search adds the collect margin (file header)
+  const long long slack = p.c8_slack + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);
+  const float inv_unit = p.c8_scale;
+  const int lc_min = -p.c8_rneg - 1;
 
   for (;;) {
     unsigned long long base = 0;
@@ -198,9 +207,9 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
         outer_flip<B, L, B>(p, B + r, sg, V, H, F);
       }
       if constexpr (LO <= 6) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
-      // the block's limit in coarse units relative to its base (floor); no limit yet: everything passes
-      const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
-      const int lc = (int)min(max(lrel, lc_min), -1ll);
+      // the block's limit in coarse units relative to its base; no limit yet: everything passes
+      const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
+      const int lc = min(max(lrel, lc_min), -1);
       unsigned a[2];
       coarse8_block_and<CB1, CB2, false, APPROX>(p, H, 0.f, 127 - lc, a);
       if (lrel < 0 && (a[0] & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
@@ -239,9 +248,9 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
   const int lane = threadIdx.x & 31;
-  const long long slack = ((long long)(B + 2) << p.c8_shift >> 1) + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);
-  const int sh = p.c8_shift;
-  const long long lc_min = -(long long)p.c8_rneg - 1;
+  const long long slack = p.c8_slack + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);  // (11+1)/2 coarse units
+  const float inv_unit = p.c8_scale;
+  const int lc_min = -p.c8_rneg - 1;
 
   for (;;) {
     unsigned long long base = 0;
@@ -273,8 +282,8 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
         outer_flip<B, L, B + 1>(p, B + 1 + r, sg, V, H, F);
       }
       if constexpr (LS <= 5) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
-      const long long lrel = thr > LLONG_MAX - slack ? 0ll : ((thr + slack - V) >> sh);
-      const int lc = (int)min(max(lrel, lc_min), -1ll);
+      const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
+      const int lc = min(max(lrel, lc_min), -1);
       unsigned a[2];
       coarse8_block_and<CB1, CB2, true, APPROX>(p, H, F[0], 127 - lc, a);
       if (lrel < 0 && (a[0] & a[1] & 0x80808080u) == 0x80808080u) continue;  // neither half holds a state under the limit

@@ -102,12 +102,15 @@ struct alignas(16) TableParams {
   unsigned long long list_cap;
   const double* coeffs64;          // original fp64 coefficients (device), for the overflow reduction
   unsigned long long* red;         // [0] best ordered value, [1] best tie key (overflow reduction)
-  // byte-packed threshold pass (qb_coarse8.cuh): coarse unit 2^c8_shift quantized units, and the bound
-  // Rneg on how far below its base a block's coarse values can reach (limits are clamped at -Rneg - 1)
+  // byte-packed threshold pass (qb_coarse8.cuh): coarse unit U quantized units (any real U >= 1, not only
+  // powers of two), c8_scale = fl(1/U); c8_slack = the certified rounding margin ceil(U ((NB+1)/2 + 0.02)) in
+  // quantized units (NB image bits); Rneg = how far below its base a block's tested values can reach (limits
+  // are clamped at -Rneg - 1); c8_zero = 0, opaque to the compiler (ALU-pipe 3-input adds)
   float c8_scale;
-  int c8_shift;
   int c8_rneg;
+  int c8_zero;
   int c8_pad;
+  long long c8_slack;
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };
