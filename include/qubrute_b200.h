@@ -81,7 +81,9 @@ typedef struct qb_result {
   uint64_t param_bytes;   /* bytes of kernel parameters copied host->device per launch (Q, T tables) */
   double module_ms;       /* host time patching + loading the patched-immediate kernel (0: cached / not used) */
   int32_t combine;        /* qb_solve_devices: 1 = shards combined by one ncclAllReduce, 0 = on the host */
-  int32_t reserved;
+  int32_t retries;        /* AUTO: optimistic runs of a faster kernel that gave up before this one completed */
+  uint64_t exact_blocks;  /* byte-packed threshold kernels: blocks that failed the byte test and were re-evaluated
+                             exactly (the rest were certified above the running best), else 0 */
 } qb_result;
 
 /* Library / device management. */

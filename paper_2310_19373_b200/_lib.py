@@ -90,7 +90,8 @@ class QbResult(ctypes.Structure):
         ("param_bytes", ctypes.c_uint64),
         ("module_ms", ctypes.c_double),
         ("combine", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("retries", ctypes.c_int32),
+        ("exact_blocks", ctypes.c_uint64),
     ]
 
 

@@ -117,6 +117,7 @@ constexpr int kImmSeen = 16;
 struct ImmModule {
   int L = 0;
   unsigned long long hash = 0;   // FNV-1a of the patched table words
+  unsigned long long inst = 0;   // instance_key of the AUTO solve that loaded it (0: explicit variant)
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
   unsigned long long last_use = 0;
@@ -137,7 +138,8 @@ struct Device {
   unsigned long long* d_cand = nullptr;
   size_t cand_cap = 0;
   // [0] chunk counter, [1] device-wide best (gbest_enc), [2] CTAs done, [3..5] collect counts
-  // (chunks, blocks, candidates): one zero memset before each search
+  // (chunks, blocks, candidates), [6] blocks the byte-packed kernels re-evaluated exactly, [7] their "gave up"
+  // flag: one zero memset before each search
   unsigned long long* d_work = nullptr;
   unsigned long long* d_counts = nullptr;  // = d_work + 3
   // pinned readback, one copy per solve: [0..2] collect counts, then up to kCandPre candidates
@@ -148,6 +150,7 @@ struct Device {
   size_t coeffs_cap = 0;
   unsigned long long* d_red = nullptr;     // [0] value key, [1] tie key
   unsigned long long* h_red = nullptr;     // pinned
+  unsigned long long* h_pass = nullptr;    // pinned readback of d_work[6..7]
   double* d_batch_coeffs = nullptr;
   size_t batch_coeffs_cap = 0;
   BatchOut* d_batch_out = nullptr;
@@ -165,6 +168,12 @@ struct Device {
   unsigned long long imm_clock = 0;
   unsigned long long imm_seen[kImmSeen] = {};  // table hashes solved recently (AUTO loads on a repeat)
   unsigned imm_seen_next = 0;
+  struct ImmPref {
+    unsigned long long key;
+    int kind;
+  };
+  ImmPref imm_pref[kImmSeen] = {};  // instance -> patched kernel kind that completed its last AUTO solve
+  unsigned imm_pref_next = 0;
   std::mutex mu;
 };
 
@@ -187,11 +196,12 @@ static int get_device(Device** out) {
     QB_CUDA(cudaEventCreate(&d->evs));
     QB_CUDA(cudaMalloc(&d->d_final, sizeof(FinalOut)));
     QB_CUDA(cudaMallocHost(&d->h_final, sizeof(FinalOut)));
-    QB_CUDA(cudaMalloc(&d->d_work, 6 * sizeof(unsigned long long)));
+    QB_CUDA(cudaMalloc(&d->d_work, 8 * sizeof(unsigned long long)));
     d->d_counts = d->d_work + 3;
     QB_CUDA(cudaMallocHost(&d->h_counts, (3 + kCandPre) * sizeof(unsigned long long)));
     QB_CUDA(cudaMalloc(&d->d_red, 2 * sizeof(unsigned long long)));
     QB_CUDA(cudaMallocHost(&d->h_red, 2 * sizeof(unsigned long long)));
+    QB_CUDA(cudaMallocHost(&d->h_pass, 2 * sizeof(unsigned long long)));
     g_devs[dev] = std::move(d);
   }
   *out = g_devs[dev].get();
@@ -325,7 +335,7 @@ static unsigned long long imm_hash(int kind, int L, const unsigned* words, int n
 // search); a table already loaded, or one solved before on this device, always does.
 static bool imm_auto(Device* dev, int L, unsigned long long h, double est_ms) {
   for (auto& m : dev->imm)
-    if (m.lib && m.L == L && m.hash == h) return true;
+    if (m.lib && m.L == L && m.inst == h) return true;
   bool seen = false;
   for (unsigned long long x : dev->imm_seen) seen |= (x == h);
   if (!seen) dev->imm_seen[dev->imm_seen_next++ % kImmSeen] = h;
@@ -335,12 +345,13 @@ static bool imm_auto(Device* dev, int L, unsigned long long h, double est_ms) {
 }
 
 static int imm_kernel(Device* dev, int kind, int L, const unsigned* words, int nwords, cudaKernel_t* out,
-                      bool* loaded) {
+                      bool* loaded, unsigned long long inst = 0) {
   const unsigned long long h = imm_hash(kind, L, words, nwords);
   *loaded = false;
   for (auto& m : dev->imm)
     if (m.lib && m.L == L && m.hash == h) {
       m.last_use = ++dev->imm_clock;
+      if (inst) m.inst = inst;
       *out = m.kern;
       return QB_OK;
     }
@@ -369,6 +380,7 @@ static int imm_kernel(Device* dev, int kind, int L, const unsigned* words, int n
   }
   slot->L = L;
   slot->hash = h;
+  slot->inst = inst;
   slot->last_use = ++dev->imm_clock;
   *out = slot->kern;
   *loaded = true;
@@ -381,11 +393,39 @@ static bool imm_enabled() {
 }
 
 #ifndef QB_IMM_AUTO_KIND
-#define QB_IMM_AUTO_KIND 4  // AUTO's patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3 ms), 3 = byte-packed threshold pass (22.7 ms), 4 = its super-blocks (21.7 ms)
+#define QB_IMM_AUTO_KIND 6  // AUTO's patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3 ms), 3 = byte-packed threshold pass (22.7 ms), 4 = its super-blocks (21.7 ms)
 #endif
-static int imm_auto_kind() {
+#ifndef QB_IMM8_ABORT_SHIFT
+#define QB_IMM8_ABORT_SHIFT 10  // AUTO: a byte-packed kernel gives up beyond 1 exact re-evaluation per 2^10 blocks (~ +10% time)
+#endif
+// FNV-1a over the coefficients: identifies an instance across AUTO solves (module cache, kernel preference)
+static unsigned long long instance_key(const double* c, int n, int L) {
+  unsigned long long h = 1469598103934665603ull ^ (unsigned long long)L ^ ((unsigned long long)n << 32);
+  for (size_t t = 0; t < (size_t)n * n; ++t) {
+    unsigned long long w;
+    std::memcpy(&w, &c[t], 8);
+    h = (h ^ w) * 1099511628211ull;
+  }
+  return h ? h : 1ull;
+}
+// AUTO's patched kernel for an instance: QB_IMM_KIND if set; else the kind a retry asks for; else the kind that
+// completed the last solve of this instance on this device; else the fastest (QB_IMM_AUTO_KIND)
+static int imm_auto_kind(Device* dev, unsigned long long key, int forced) {
   const char* e = std::getenv("QB_IMM_KIND");
-  return e ? std::atoi(e) : QB_IMM_AUTO_KIND;
+  if (e) return std::atoi(e);
+  if (forced) return forced;
+  for (auto& pr : dev->imm_pref)
+    if (pr.key == key && key) return pr.kind;
+  return QB_IMM_AUTO_KIND;
+}
+static void imm_set_pref(Device* dev, unsigned long long key, int kind) {
+  if (!key) return;
+  for (auto& pr : dev->imm_pref)
+    if (pr.key == key) {
+      pr.kind = kind;
+      return;
+    }
+  dev->imm_pref[dev->imm_pref_next++ % kImmSeen] = {key, kind};
 }
 
 // ------------------------------------------------------------------ NCCL combine (qb_solve_devices)
@@ -444,6 +484,8 @@ struct Plan {
   KernelSet* ks = nullptr;
   std::unique_ptr<TableParams> P;
   std::vector<unsigned> imm2_words;  // 11-bit coarse table (super-block kernel), 1024 packed words
+  int m_fix = 0;                     // fixed high bits and their value: the host seed stays inside this subspace
+  unsigned long long suffix = 0;
   std::vector<unsigned> imm8_words;  // byte-packed coarse table (threshold kernel), 256 words; empty: not built
 };
 
@@ -453,7 +495,7 @@ static double sym(const double* c, int n, int i, int j) {
 
 // Integer scaling: q = rint(c * 2^e) with every partial sum the device forms below 2^24.
 // BE: block bits (their relative values are formed in fp32); B: table bits (T is built over them).
-static long long seed_greedy(const std::vector<double>& q, int n);
+static long long seed_greedy(const std::vector<double>& q, int n, int m_fix, unsigned long long suffix);
 
 static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_image = false, bool seed = false,
                     bool imm2_image = false, int imm8_image = 0) {
@@ -546,7 +588,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
 #endif
   while (std::ldexp(rq_in, -cs) + B + 2 > field_max) ++cs;
   P.coarse_shift = cs;
-  P.seed_val = seed ? seed_greedy(q, n) : LLONG_MAX;  // whole-space coarse searches only
+  P.seed_val = seed ? seed_greedy(q, n, pl.m_fix, pl.suffix) : LLONG_MAX;  // a value attained inside the searched subspace
   P.coarse_scale = (float)std::ldexp(1.0, -cs);
   const int bias = (int)field_max + 1;
   const double cscale = std::ldexp(1.0, -cs);  // exact power of two: x * cscale == ldexp(x, -cs)
@@ -586,7 +628,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
   P.c8_scale = 1.f;
   P.c8_rneg = 0;
   P.c8_zero = 0;
-  P.c8_pad = 0;
+  P.c8_abort_shift = -1;
   P.c8_slack = 0;
   if (imm8_image && B == BMAX && ((imm8_image & 3) == 1 || n > B)) {
     // byte image of the threshold kernels (qb_coarse8.cuh); (imm8_image & 3) == 2: the super-block form, whose
@@ -701,8 +743,11 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
 
 // Greedy 1-flip descent on the quantized instance from a few starts: an attained value to start the
 // coarse kernel's pruning from (exact int64 arithmetic, O(n) per flip).  Only valid when the search
-// covers the whole space (the seed state must lie in it).
-static long long seed_greedy(const std::vector<double>& q, int n) {
+// covers the whole space (the seed state must lie in it); with m_fix high bits fixed to `suffix` the descent
+// only flips the free bits, so the seed lies in that subspace.
+static long long seed_greedy(const std::vector<double>& q, int n, int m_fix, unsigned long long suffix) {
+  const int nfree = n - m_fix;
+  const unsigned long long fixed = m_fix > 0 ? suffix << nfree : 0ull;
   long long seed = LLONG_MAX;
   std::vector<long long> qi((size_t)n * n);
   for (size_t t = 0; t < qi.size(); ++t) qi[t] = (long long)q[t];
@@ -720,7 +765,7 @@ static long long seed_greedy(const std::vector<double>& q, int n) {
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
       x = z ^ (z >> 31);
     }
-    x &= mask64(n);
+    x = (x & mask64(nfree)) | fixed;
     long long v = 0;
     std::vector<long long> fld(n);  // fld[i] = q_ii + sum_{j != i} q_ij x_j (gain of setting bit i)
     for (int i = 0; i < n; ++i) {
@@ -738,7 +783,7 @@ static long long seed_greedy(const std::vector<double>& q, int n) {
     for (int it = 0; it < 4 * n; ++it) {
       int bi = -1;
       long long bd = 0;
-      for (int i = 0; i < n; ++i) {
+      for (int i = 0; i < nfree; ++i) {
         const long long d = ((x >> i) & 1ull) ? -fld[i] : fld[i];
         if (d < bd) { bd = d; bi = i; }
       }
@@ -846,7 +891,7 @@ static double eval_bits(const double* c, int n, unsigned long long x) {
 #endif
 static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long suffix, int m_tie, int rule,
                       uint32_t shard, uint32_t shard_count, int variant, qb_result* out,
-                      std::vector<unsigned long long>* all_out = nullptr) {
+                      std::vector<unsigned long long>* all_out = nullptr, int auto_kind = 0, int retries = 0) {
   auto t_start = std::chrono::steady_clock::now();
   if (!coeffs || !out) return fail(QB_E_ARG, "null pointer");
   if (n < 1) return fail(QB_E_ARG, "dimension must be at least 1");
@@ -863,7 +908,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
-  std::lock_guard<std::mutex> guard(dev->mu);
+  std::unique_lock<std::mutex> guard(dev->mu);
   QB_TMARK("device");
 
   Plan pl;
@@ -893,6 +938,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   // runs, unless QB_IMM=0); QB_VARIANT_COARSE forces the table-load coarse kernel.  Kind 2 = the 11-bit
   // super-block kernel (needs L >= B + 2), AUTO's kind unless QB_IMM_KIND=1.
   bool imm = coarse && (variant >= QB_VARIANT_IMM || (variant == QB_VARIANT_AUTO && imm_enabled()));
+  // AUTO: the instance's identity for the module / preference caches (the tables depend on coeffs and L only)
+  const unsigned long long inst_key = (imm && variant == QB_VARIANT_AUTO) ? instance_key(coeffs, n, L) : 0ull;
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit kernel, reported as IMM)
   int imm_kind = !imm                                ? 0
                  : variant == QB_VARIANT_IMM         ? 1
@@ -900,16 +947,18 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
                  : variant == QB_VARIANT_IMM8S       ? 4
                  : variant == QB_VARIANT_IMM8A       ? 5
                  : variant == QB_VARIANT_IMM8AS      ? 6
-                 : variant == QB_VARIANT_AUTO        ? imm_auto_kind()
+                 : variant == QB_VARIANT_AUTO        ? imm_auto_kind(dev, inst_key, auto_kind)
                                                      : 2;
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit form of the same pass)
   if (imm_kind == 2 && L < BMAX + 2) imm_kind = 1;
   if (imm8_super(imm_kind) && L < BMAX + 2) imm_kind -= 1;
   QB_TMARK("geometry");
-  // the host seed must be a value some searched state attains: whole-space searches (m_fix == 0) of the
-  // coarse and tensor-core kernels, any chunk length; shards use it too (the combine treats a shard
-  // that finds nothing <= the seed as empty, see the shard handling below)
-  const bool seed = (coarse || tc) && m_fix == 0 && n >= 24;
+  // the host seed must be a value some searched state attains: the greedy descent keeps the m_fix fixed bits
+  // at `suffix`, so it lies in the searched subspace (coarse and tensor-core kernels, any chunk length);
+  // shards use it too (the combine treats a shard that finds nothing <= the seed as empty, see below)
+  const bool seed = (coarse || tc) && n - m_fix >= 24;
+  pl.m_fix = m_fix;
+  pl.suffix = suffix;
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2,
                         imm_kind < 3 ? 0 : (imm8_super(imm_kind) ? 2 : 1) | (imm8_approx(imm_kind) ? 4 : 0)))
     return rc;
@@ -941,13 +990,16 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   cudaKernel_t imm_fn = nullptr;
   if (imm && variant == QB_VARIANT_AUTO) {
     const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 3.0e13 * 1e3;
-    imm = imm_auto(dev, L, imm_hash(imm_kind, L, imm_words, imm_nwords), est_ms);
+    imm = imm_auto(dev, L, inst_key, est_ms);
+    // AUTO runs the byte-packed kernels optimistically: one that has to re-evaluate more than 1 block in 2^10
+    // exactly gives up and the solve is re-run with the next tighter kernel (6 -> 5 -> 3 -> 1), see below
+    if (imm && imm_kind >= 3) P.c8_abort_shift = QB_IMM8_ABORT_SHIFT;
   }
   double module_ms = 0.0;
   if (imm) {
     bool loaded = false;
     const auto tm0 = std::chrono::steady_clock::now();
-    const int rc_imm = imm_kernel(dev, imm_kind, L, imm_words, imm_nwords, &imm_fn, &loaded);
+    const int rc_imm = imm_kernel(dev, imm_kind, L, imm_words, imm_nwords, &imm_fn, &loaded, inst_key);
     if (loaded) module_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
     if (int rc = rc_imm) {
       if (variant != QB_VARIANT_AUTO) return rc;
@@ -1032,7 +1084,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   cudaStream_t st = dev->stream;
   // chunk counter, device-wide best (+infinity), done counter and collect counts in one memset
-  QB_CUDA(cudaMemsetAsync(dev->d_work, 0, 6 * sizeof(unsigned long long), st));
+  QB_CUDA(cudaMemsetAsync(dev->d_work, 0, 8 * sizeof(unsigned long long), st));
   QB_TMARK("memsets");
   QB_CUDA(cudaEventRecord(dev->ev0, st));
   if (imm) {
@@ -1074,6 +1126,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   QB_CUDA(cudaEventRecord(dev->ev1, st));
   // one readback: the search result, and on the collect path the counts plus the first candidates
   QB_CUDA(cudaMemcpyAsync(dev->h_final, dev->d_final, sizeof(FinalOut), cudaMemcpyDeviceToHost, st));
+  dev->h_pass[0] = dev->h_pass[1] = 0;
+  if (imm_kind >= 3)
+    QB_CUDA(cudaMemcpyAsync(dev->h_pass, dev->d_work + 6, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   if (collect) {
     QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     QB_CUDA(cudaMemcpyAsync(dev->h_counts + 3, dev->d_cand,
@@ -1090,6 +1145,24 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->search_ms = ms;
   out->collect_ms = collect ? out->kernel_ms - out->search_ms : 0.0;
   const FinalOut fo = *dev->h_final;
+  out->exact_blocks = dev->h_pass[0];
+  out->retries = retries;
+  if (imm && imm_kind >= 3 && P.c8_abort_shift >= 0 && dev->h_pass[1] != 0) {
+    // the optimistic byte-packed kernel gave up (too many blocks failed its test): nothing of this run is
+    // used; run the next tighter kernel.  The device time spent is charged to the result.
+    const int next = imm_kind == 6 ? 5 : imm_kind == 5 ? 3 : imm_kind == 4 ? 3 : 1;
+    const double spent_kernel = out->kernel_ms;
+    const double spent_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    guard.unlock();
+    if (int rc = solve_impl(coeffs, n, m_fix, suffix, m_tie, rule, shard, shard_count, variant, out, all_out, next,
+                            retries + 1))
+      return rc;
+    out->kernel_ms += spent_kernel;
+    out->search_ms += spent_kernel;
+    out->total_ms += spent_total;
+    return QB_OK;
+  }
+  if (imm && variant == QB_VARIANT_AUTO) imm_set_pref(dev, inst_key, imm_kind);
   if (!fo.found) {
     if (seed && shard_count > 1 && fo.val == LLONG_MAX) {
       // every block of this shard was certified above the seed value, which some state of another shard
@@ -1468,6 +1541,7 @@ void qb_shutdown(void) {
     cudaFree(d->d_coeffs);
     cudaFree(d->d_red);
     cudaFreeHost(d->h_red);
+    cudaFreeHost(d->h_pass);
     cudaFree(d->d_batch_coeffs);
     cudaFree(d->d_batch_out);
     cudaFreeHost(d->h_batch_stage);

@@ -47,6 +47,9 @@
 #ifndef QB_IMM8A_ALU
 #define QB_IMM8A_ALU 4  // row-bound form: of the 16 adds of a row, those issued as IADD3 on the ALU pipe (the rest: IMAD)
 #endif
+#ifndef QB_IMM8_ABORT_ALLOWANCE
+#define QB_IMM8_ABORT_ALLOWANCE (1ull << 14)  // exact re-evaluations allowed before the optimistic run may give up
+#endif
 #ifndef QB_IMM8_MINB
 #define QB_IMM8_MINB 4
 #endif
@@ -178,12 +181,24 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
   const int lc_min = -p.c8_rneg - 1;
 
   for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(p.work, 32ull);
+    unsigned long long base = 0, passed = 0;
+    if (lane == 0) {
+      base = atomicAdd(p.work, 32ull);
+      passed = __ldcg(p.work + 6);
+    }
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= nchunks) break;
+    if (p.c8_abort_shift >= 0) {
+      // AUTO's optimistic run: too many blocks are failing the byte test for it to pay (warp-uniform decision)
+      passed = __shfl_sync(0xffffffffu, passed, 0);
+      if (passed > ((base << LO) >> p.c8_abort_shift) + QB_IMM8_ABORT_ALLOWANCE) {
+        if (lane == 0) p.work[7] = 1ull;
+        break;
+      }
+    }
     const unsigned long long ci = base + lane;
     if (ci >= nchunks) continue;
+    unsigned npass = 0;
     const unsigned long long c = p.chunk_begin + ci;
     const unsigned long long s = chunk_prefix(p, c);
     long long V;
@@ -206,13 +221,15 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
         const float sg = ((j >> (r + 1)) & 1u) ? -1.f : 1.f;
         outer_flip<B, L, B>(p, B + r, sg, V, H, F);
       }
-      if constexpr (LO <= 6) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+      // device-wide best: refreshed every block in short chunks, every 64 blocks in long ones
+      if (LO <= 6 || (j & 63u) == 0u) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
       // the block's limit in coarse units relative to its base; no limit yet: everything passes
       const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
       const int lc = min(max(lrel, lc_min), -1);
       unsigned a[2];
       coarse8_block_and<CB1, CB2, false, APPROX>(p, H, 0.f, 127 - lc, a);
       if (lrel < 0 && (a[0] & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
+      ++npass;
       const long long val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
       cmin = min(cmin, val);
       if (val <= best.val) {
@@ -225,6 +242,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
       }
     }
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
+    if (npass) atomicAdd(p.work + 6, (unsigned long long)npass);
   }
   // records only: the reduction runs as finalize_kernel (qb_table.cuh)
   const Rec r = cta_reduce<TPB>(best);
@@ -253,12 +271,24 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
   const int lc_min = -p.c8_rneg - 1;
 
   for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(p.work, 32ull);
+    unsigned long long base = 0, passed = 0;
+    if (lane == 0) {
+      base = atomicAdd(p.work, 32ull);
+      passed = __ldcg(p.work + 6);
+    }
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= nchunks) break;
+    if (p.c8_abort_shift >= 0) {
+      // AUTO's optimistic run: too many blocks are failing the byte test for it to pay (warp-uniform decision)
+      passed = __shfl_sync(0xffffffffu, passed, 0);
+      if (passed > ((base << LO) >> p.c8_abort_shift) + QB_IMM8_ABORT_ALLOWANCE) {
+        if (lane == 0) p.work[7] = 1ull;
+        break;
+      }
+    }
     const unsigned long long ci = base + lane;
     if (ci >= nchunks) continue;
+    unsigned npass = 0;
     const unsigned long long c = p.chunk_begin + ci;
     const unsigned long long s = chunk_prefix(p, c);
     long long V;
@@ -281,7 +311,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
         const float sg = ((jp >> (r + 1)) & 1u) ? -1.f : 1.f;
         outer_flip<B, L, B + 1>(p, B + 1 + r, sg, V, H, F);
       }
-      if constexpr (LS <= 5) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+      if (LS <= 5 || (jp & 31u) == 0u) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
       const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
       const int lc = min(max(lrel, lc_min), -1);
       unsigned a[2];
@@ -291,6 +321,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
       for (int t = 0; t < 2; ++t) {
         const int b = t ^ (int)(jp & 1u);  // half evaluated in original block order j = 2 jp + t
         if (lrel < 0 && ((b ? a[1] : a[0]) & 0x80808080u) == 0x80808080u) continue;
+        ++npass;
         // exact fp32 table evaluation from the half's own base: (V, H) or (V + q_BB + F_B, H + q_.B)
         float Hb[B];
 #pragma unroll
@@ -310,6 +341,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
       }
     }
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
+    if (npass) atomicAdd(p.work + 6, (unsigned long long)npass);
   }
   const Rec r = cta_reduce<TPB>(best);
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;

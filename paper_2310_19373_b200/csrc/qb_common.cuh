@@ -93,7 +93,8 @@ struct alignas(16) TableParams {
   unsigned long long cand_cap;
   Rec* cta_out;                    // one record per CTA
   FinalOut* final_out;
-  unsigned long long* work;        // dynamic chunk counter (zeroed before each search launch)
+  unsigned long long* work;        // dynamic chunk counter (zeroed before each search launch); byte-packed
+                                   // kernels: work[6] = blocks re-evaluated exactly, work[7] = gave up (AUTO)
   unsigned long long* gbest;       // device-wide best value so far, gbest_enc() form (0 = +infinity)
   unsigned long long* done;        // CTAs finished (the last one reduces the records), zeroed per launch
   unsigned long long* counts;      // collect pass counters: [0] chunks, [1] blocks, [2] unused
@@ -106,10 +107,13 @@ struct alignas(16) TableParams {
   // powers of two), c8_scale = fl(1/U); c8_slack = the certified rounding margin ceil(U ((NB+1)/2 + 0.02)) in
   // quantized units (NB image bits); Rneg = how far below its base a block's tested values can reach (limits
   // are clamped at -Rneg - 1); c8_zero = 0, opaque to the compiler (ALU-pipe 3-input adds)
+  // c8_abort_shift >= 0: AUTO's optimistic run -- the kernel gives up (work[7] = 1) once the blocks it had
+  // to re-evaluate exactly (work[6]) exceed blocks_started >> c8_abort_shift plus a start-up allowance, and the
+  // host re-runs the solve with a tighter kernel; negative: never
   float c8_scale;
   int c8_rneg;
   int c8_zero;
-  int c8_pad;
+  int c8_abort_shift;
   long long c8_slack;
 };
 
@@ -128,7 +132,8 @@ __device__ __forceinline__ long long gbest_dec(unsigned long long e) {
 // margin; read from the device so the collect pass is enqueued without a host round trip.
 __device__ __forceinline__ long long collect_theta(const TableParams& p) {
   const long long v = __ldcg(&p.final_out->val);
-  return v == LLONG_MAX ? LLONG_MIN : v + p.theta_add;  // LLONG_MAX: the search found nothing (empty shard)
+  // LLONG_MAX: the search found nothing (empty shard); work[7]: the search gave up (AUTO re-runs it): list nothing
+  return (v == LLONG_MAX || __ldcg(p.work + 7) != 0ull) ? LLONG_MIN : v + p.theta_add;
 }
 enum { MODE_SEARCH = 0, MODE_SEARCH_RECORD = 1, MODE_COLLECT = 2, MODE_REDUCE_VALUE = 3, MODE_REDUCE_KEY = 4 };
 

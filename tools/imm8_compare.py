@@ -20,5 +20,5 @@ for n in ns:
         out[label] = (r.argmin_bits, r.value, r.candidates)
         print(f"{name} n={n} {label:5s} search {statistics.median(x.search_ms for x in rs):.3f} ms  kernel "
               f"{statistics.median(x.kernel_ms for x in rs):.3f} ms  total {statistics.median(x.total_ms for x in rs):.3f} ms  "
-              f"argmin {hex(r.argmin_bits)} value {r.value!r} cand {r.candidates} variant {r.variant}", flush=True)
+              f"argmin {hex(r.argmin_bits)} value {r.value!r} cand {r.candidates} variant {r.variant} exact_blocks {r.exact_blocks} of {2 ** (n - 10)}", flush=True)
     print("MATCH" if all(v == out["imm"] for v in out.values()) else f"MISMATCH {out}", flush=True)
