@@ -106,9 +106,10 @@ def imm_sass_sha256(L: int, kind: int = 1):
 
 
 def imm_symbol(L: int, kind: int = 1) -> str:
-    if kind >= 3:  # byte-packed threshold kernels: 3 + super-block + 2 * row-bound form
-        fam = "15coarse8s_kernel" if kind in (4, 6) else "14coarse8_kernel"
-        return f"_ZN2qb{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}EEEvNS_11TableParamsE"
+    if kind >= 3:  # byte-packed threshold kernels: 3 + super-block + 2 * row-bound form; 7: row-bound, 12-bit blocks
+        nx = {4: 1, 6: 1, 7: 2}.get(kind, 0)
+        fam, tail = ("15coarse8s_kernel", f"Li{nx}E") if nx else ("14coarse8_kernel", "")
+        return f"_ZN2qb{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}E{tail}EEvNS_11TableParamsE"
     if kind == 2:
         return f"_ZN2qb14coarse2_kernelILi5ELi5ELi{L}ELi128EEEvNS_11TableParamsE"
     return f"_ZN2qb13coarse_kernelILi5ELi5ELi4ELi6ELi{L}ELi128ELb1EEEvNS_11TableParamsE"
@@ -149,7 +150,8 @@ def fp32_lane_peak_per_sm_clk():
 
 FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel", 5: "coarse_kernel (imm)",
             6: "coarse2_kernel (imm)", 7: "coarse8_kernel (imm)", 8: "coarse8s_kernel (imm)",
-            9: "coarse8_kernel (imm, row-bound)", 10: "coarse8s_kernel (imm, row-bound)"}
+            9: "coarse8_kernel (imm, row-bound)", 10: "coarse8s_kernel (imm, row-bound)",
+            11: "coarse8s_kernel (imm, row-bound, 12-bit)"}
 
 
 def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path):
@@ -560,12 +562,12 @@ def main():
         # kernel and the literal per-step field walk (QB_VARIANT_COARSE / _TABLE / _FIELDWALK)
         names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse_tableload", 4: "tc", 5: "coarse_imm",
                  6: "coarse_imm_superblock", 7: "threshold_imm8", 8: "threshold_imm8_superblock", 9: "threshold_imm8_rowbound",
-                 10: "threshold_imm8_rowbound_superblock"}
+                 10: "threshold_imm8_rowbound_superblock", 11: "threshold_imm8_rowbound_12bit"}
         line["variants"] = {f"{names[int(r.variant)]} (default)": {
             "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
         # (the tensor-core pass, QB_VARIANT_TC, is retired from this list: 40 ms, TMEM round-trip bound,
         # DESIGN.md section 4)
-        for var in (_lib.VARIANT_IMM8AS, _lib.VARIANT_IMM8A, _lib.VARIANT_IMM8S, _lib.VARIANT_IMM8, _lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE,
+        for var in (_lib.VARIANT_IMM8AQ, _lib.VARIANT_IMM8AS, _lib.VARIANT_IMM8A, _lib.VARIANT_IMM8S, _lib.VARIANT_IMM8, _lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE,
                     _lib.VARIANT_FIELDWALK):
             _lib.solve(inst.coeffs, variant=var)
             vr = _lib.solve(inst.coeffs, variant=var)

@@ -57,6 +57,8 @@ extern "C" {
 #define QB_VARIANT_IMM8A 9     /* row-bound form of IMM8: every row of a block is tested with the least row term
                                   (a certified lower bound of each state), one 2-input add per four states */
 #define QB_VARIANT_IMM8AS 10   /* row-bound form of IMM8S */
+#define QB_VARIANT_IMM8AQ 11   /* row-bound form over 12-bit super-blocks (four blocks per pass, chunks of >= 13
+                                  free bits); AUTO's first choice where the coarse filter runs */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {
@@ -104,7 +106,11 @@ double qb_eval_upper(const double* coeffs, int n, const double* x);
  *   m_tie      tie rule parameter for QB_TIE_GRAY (m_fix <= m_tie < n): 0 = solve_incremental,
  *              m = solve_parallel(fixed_bits=m); for solve_subspace pass m_tie = m_fix
  *   shard, shard_count   scan only shard `shard` of `shard_count` equal slices of the chunk space
- *              (multi-GPU: one shard per rank; combine results by (value_key, tie_key))
+ *              (multi-GPU: one shard per rank; combine results by (value_key, tie_key)).  With
+ *              shard_count > 1 only the COMBINED result is the solve's answer: every shard prunes against one
+ *              host-found attained value of the whole searched space, so a shard that holds neither the minimum
+ *              nor a tie may return an empty result (keys ~0, value NaN) or an attained value above its own
+ *              minimum; a shard that holds the minimum or a tie always returns it exactly.
  * Replaces solver._scan_subspace + _kernels.gray_scan (solver.py:159-170, _kernels.py:46-75)
  * and the thread-pool fan-out + combine_subspace_minima of solve_parallel (solver.py:193-229). */
 int qb_solve(const double* coeffs, int n, int m_fix, uint64_t suffix, int m_tie, int tie_rule,
@@ -160,13 +166,13 @@ int qb_prefix_eval(const double* coeffs, int n, int k, uint64_t c_begin, uint64_
                    double* fields);
 
 /* Test hook (host only): the embedded patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 512 coarse
- * table words; 2: QB_VARIANT_IMM2, 1024 words; 3 / 5: QB_VARIANT_IMM8 / IMM8A, 256 words; 4 / 6: QB_VARIANT_IMM8S / IMM8AS, 512 words) for chunk length L with `words` written into its
+ * table words; 2: QB_VARIANT_IMM2, 1024 words; 3 / 5: QB_VARIANT_IMM8 / IMM8A, 256 words; 4 / 6: QB_VARIANT_IMM8S / IMM8AS, 512 words; 7: QB_VARIANT_IMM8AQ, 1024 words) for chunk length L with `words` written into its
  * placeholder immediates -- the image those variants load.
  * *size receives the image size; the image is copied to `out` when cap >= *size. */
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size);
 
-/* Test hook (host only): the byte image the threshold kernels (kind 3..6 = QB_VARIANT_IMM8, IMM8S, IMM8A, IMM8AS)
- * would run `coeffs` with: the packed table words (256 for kinds 3 / 5, 512 for 4 / 6), the quantized upper-
+/* Test hook (host only): the byte image the threshold kernels (kind 3..7 = QB_VARIANT_IMM8, IMM8S, IMM8A, IMM8AS, IMM8AQ)
+ * would run `coeffs` with: the packed table words (256 for kinds 3 / 5, 512 for 4 / 6, 1024 for 7), the quantized upper-
  * triangular instance (n * n doubles, integer-valued, coefficient * 2^scale_exp rounded), fl(1 / unit), the range
  * bound Rneg and the certified rounding margin (quantized units).  tests/test_byte_image_cpu.py replays the
  * device's block test on it and checks the range and no-false-negative claims of qb_coarse8.cuh. */

@@ -30,7 +30,8 @@ IMM2_LS = (12, 13, 14, 16, 18, 20, 22)  # super-block kernel: chunks of >= B + 2
 IMM8_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse8_imm.cu")  # byte-packed threshold kernel
 IMM8_LS = IMM_LS
 IMM8S_LS = IMM2_LS  # its 11-bit super-block form
-IMM_WORDS = {1: 512, 2: 1024, 3: 256, 4: 512, 5: 256, 6: 512}  # placeholder immediates per patched kernel kind
+IMM8Q_LS = (13, 14, 16, 18, 20, 22)  # 12-bit super-blocks: chunks of >= B + 3 free bits
+IMM_WORDS = {1: 512, 2: 1024, 3: 256, 4: 512, 5: 256, 6: 512, 7: 1024}  # placeholder immediates per patched kernel kind
 
 QB_OK = 0
 QB_E_ARG = -1
@@ -53,6 +54,10 @@ VARIANT_IMM8 = 7
 VARIANT_IMM8S = 8
 VARIANT_IMM8A = 9
 VARIANT_IMM8AS = 10
+VARIANT_IMM8AQ = 11
+# the patched-immediate search kernels (AUTO picks among them where the coarse filter runs)
+IMM_VARIANTS = (VARIANT_IMM, VARIANT_IMM2, VARIANT_IMM8, VARIANT_IMM8S, VARIANT_IMM8A, VARIANT_IMM8AS,
+                VARIANT_IMM8AQ)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -156,12 +161,13 @@ def build(force: bool = False, verbose: bool = False, output: str | None = None,
         procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
     cubins = []
-    # kinds 3..6: byte-packed threshold kernels, 3 + super-block + 2 * row-bound form
+    # kinds 3..7: byte-packed threshold kernels (3 + super-block + 2 * row-bound form; 7: row-bound, 12-bit blocks)
     for kind, src, Ls, extra in ((1, IMM_SOURCE, IMM_LS, ()), (2, IMM2_SOURCE, IMM2_LS, ()),
                                   (3, IMM8_SOURCE, IMM8_LS, ()),
                                   (4, IMM8_SOURCE, IMM8S_LS, ("-DQB_IMM8_SUPER=1",)),
                                   (5, IMM8_SOURCE, IMM8_LS, ("-DQB_IMM8_APPROX=1",)),
-                                  (6, IMM8_SOURCE, IMM8S_LS, ("-DQB_IMM8_SUPER=1", "-DQB_IMM8_APPROX=1"))):
+                                  (6, IMM8_SOURCE, IMM8S_LS, ("-DQB_IMM8_SUPER=1", "-DQB_IMM8_APPROX=1")),
+                                  (7, IMM8_SOURCE, IMM8Q_LS, ("-DQB_IMM8_SUPER=2", "-DQB_IMM8_APPROX=1"))):
         for L in Ls:
             cub = os.path.join(objdir, f"qb_coarse_imm{kind}_L{L}.cubin")
             cmd = ["nvcc", *[f for f in compile_flags if not f.startswith("-Xcompiler") and "-fPIC" not in f],
@@ -372,7 +378,7 @@ def byte_image(coeffs, kind: int):
 
 def imm_image(L: int, words, kind: int = 1) -> bytes:
     """The patched-immediate cubin of `kind` (1: QB_VARIANT_IMM, 2: IMM2, 3: IMM8, 4: IMM8S, 5: IMM8A,
-    6: IMM8AS; IMM_WORDS[kind] table words) for chunk length L with coarse table words `words` (test hook)."""
+    6: IMM8AS, 7: IMM8AQ; IMM_WORDS[kind] table words) for chunk length L with coarse table words `words` (test hook)."""
     w = np.ascontiguousarray(words, dtype=np.uint32)
     if kind not in IMM_WORDS or w.shape != (IMM_WORDS[kind],):
         raise ValueError(f"kind {kind} needs {IMM_WORDS.get(kind)} table words")

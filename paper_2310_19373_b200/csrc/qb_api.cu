@@ -242,7 +242,7 @@ extern "C" {
 struct qb_imm_cubin {
   int kind;  // 1: coarse_kernel<.., IMM = true> (10-bit pass), 2: coarse2_kernel (11-bit super-blocks),
              // 3: coarse8_kernel (byte-packed threshold pass), 4: coarse8s_kernel (its super-block form),
-             // 5 / 6: the row-bound (APPROX) forms of 3 / 4
+             // 5 / 6: the row-bound (APPROX) forms of 3 / 4, 7: row-bound 12-bit super-blocks
   int L;
   const unsigned char* data;
   size_t size;
@@ -256,7 +256,11 @@ constexpr int kImm2Words = 1 << BMAX;       // Tc11 words = placeholders of the 
 constexpr int kImm8Words = 1 << (BMAX - 2);  // byte-packed words = placeholders of the threshold kernel
 constexpr int kImm8sWords = 1 << (BMAX - 1);  // ... of its super-block form (11 image bits)
 static int imm_nwords_of(int kind) {
-  return kind == 1 ? kImmWords : kind == 2 ? kImm2Words : (kind == 4 || kind == 6) ? kImm8sWords : kImm8Words;
+  return kind == 1   ? kImmWords
+         : kind == 2 ? kImm2Words
+         : kind == 7 ? 2 * kImm8sWords  // 12 image bits
+         : (kind == 4 || kind == 6) ? kImm8sWords
+                                    : kImm8Words;
 }
 
 // Write words[idx] into every SASS instruction whose 32-bit immediate (bits 32..63 of the first
@@ -305,15 +309,17 @@ static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words, in
   return kernels == 1;
 }
 
-// kinds 3..6 of the byte-packed threshold kernels: 3 + super + 2 * approx
-static bool imm8_super(int kind) { return kind == 4 || kind == 6; }
-static bool imm8_approx(int kind) { return kind == 5 || kind == 6; }
+// kinds 3..7 of the byte-packed threshold kernels: extra image bits NX (0: 10-bit blocks, 1 / 2: super-blocks) and
+// exact row terms or the row-bound form
+static int imm8_nx(int kind) { return kind == 7 ? 2 : (kind == 4 || kind == 6) ? 1 : 0; }
+static bool imm8_approx(int kind) { return kind >= 5 && kind <= 7; }
 static std::string imm_kernel_name(int kind, int L) {
-  if (kind >= 3)  // 3..6: coarse8[s]_kernel<..., APPROX>
-    return std::string(imm8_super(kind) ? "_ZN2qb15coarse8s_kernelILi" : "_ZN2qb14coarse8_kernelILi") +
+  if (kind >= 3)  // 3..7: coarse8_kernel<..., APPROX> / coarse8s_kernel<..., APPROX, NX>
+    return std::string(imm8_nx(kind) ? "_ZN2qb15coarse8s_kernelILi" : "_ZN2qb14coarse8_kernelILi") +
            std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" + std::to_string(QB_COARSE_B1) + "ELi" +
            std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" + std::to_string(TPB) + "ELb" +
-           (imm8_approx(kind) ? "1" : "0") + "EEEvNS_11TableParamsE";
+           (imm8_approx(kind) ? "1" : "0") + "E" + (imm8_nx(kind) ? "Li" + std::to_string(imm8_nx(kind)) + "E" : "") +
+           "EEvNS_11TableParamsE";
   if (kind == 2)
     return "_ZN2qb14coarse2_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
            std::to_string(L) + "ELi" + std::to_string(TPB) + "EEEvNS_11TableParamsE";
@@ -393,7 +399,7 @@ static bool imm_enabled() {
 }
 
 #ifndef QB_IMM_AUTO_KIND
-#define QB_IMM_AUTO_KIND 6  // AUTO's patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3 ms), 3 = byte-packed threshold pass (22.7 ms), 4 = its super-blocks (21.7 ms)
+#define QB_IMM_AUTO_KIND 7  // AUTO's patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3 ms), 3 = byte-packed threshold pass (22.7 ms), 4 = its super-blocks (21.7 ms)
 #endif
 #ifndef QB_IMM8_ABORT_SHIFT
 #define QB_IMM8_ABORT_SHIFT 10  // AUTO: a byte-packed kernel gives up beyond 1 exact re-evaluation per 2^10 blocks (~ +10% time)
@@ -630,7 +636,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
   P.c8_zero = 0;
   P.c8_abort_shift = -1;
   P.c8_slack = 0;
-  if (imm8_image && B == BMAX && ((imm8_image & 3) == 1 || n > B)) {
+  if (imm8_image && B == BMAX && n >= B + (imm8_image & 3) - 1) {
     // byte image of the threshold kernels (qb_coarse8.cuh); (imm8_image & 3) == 2: the super-block form, whose
     // image also covers bit B (NB = B + 1 image bits, fields formed from the bits above B only).
     // H_i = sum_{q >= NB} x_q q_iq lies in [hneg_i, hpos_i] for every state; the device forms
@@ -638,7 +644,7 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
     // expression at hneg_i and hpos_i (computed here in float exactly as on the device).
     // X(z) = sum_{i in z} hc_i + Tc8(z) is bounded over the 2^NB image states by doubling; the unit U is the
     // smallest of a few candidates with Rneg + Rpos <= 127.
-    const int NB = (imm8_image & 3) == 2 ? B + 1 : B;
+    const int NB = B + (imm8_image & 3) - 1;
     // row-bound form (imm8_image & 4): the row bits (QB_COARSE_B2 .. NB-1) enter every byte as the constant
     // amin = sum min(hc_i, 0) instead of their subset sums
     const bool approx8 = (imm8_image & 4) != 0;
@@ -650,18 +656,17 @@ static int quantize(const double* c, int n, int BE, int B, Plan& pl, bool tc_ima
         (v > 0 ? hpos[i] : hneg[i]) += v;
       }
     }
-    // image table over NB bits: T(z), and for the super-block T(z) + b (q_BB + sum_{i<B} z_i q_iB)
-    std::vector<double> timg((size_t)1 << NB);
-    for (int z = 0; z < (1 << B); ++z) timg[z] = (double)P.T[z];
-    if (NB > B) {
-      std::vector<double> RB((size_t)1 << B);
+    // image table over NB bits, by the doubling that builds P.T: T(z + 2^b) = T(z) + q_bb + sum_{i<b} z_i q_ib
+    std::vector<double> timg((size_t)1 << NB), RB((size_t)1 << (NB - 1));
+    timg[0] = 0.0;
+    for (int b = 0; b < NB; ++b) {
+      const double qbb = q[(size_t)b * n + b];
       RB[0] = 0.0;
-      for (int i = 0; i < B; ++i) {
-        const double qiB = q[(size_t)i * n + B];
-        for (int z = 0; z < (1 << i); ++z) RB[z + (1 << i)] = RB[z] + qiB;
+      for (int i = 0; i < b; ++i) {
+        const double qib = q[(size_t)i * n + b];
+        for (int z = 0; z < (1 << i); ++z) RB[z + (1 << i)] = RB[z] + qib;
       }
-      const double qBB = q[(size_t)B * n + B];
-      for (int z = 0; z < (1 << B); ++z) timg[(size_t)z + (1 << B)] = (double)P.T[z] + qBB + RB[z];
+      for (int z = 0; z < (1 << b); ++z) timg[(size_t)z + (1 << b)] = timg[z] + qbb + RB[z];
     }
     double tmin = 0.0, tmax = 0.0, range = 0.0;
     for (int z = 0; z < (1 << NB); ++z) {
@@ -904,7 +909,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8AS) return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8AQ) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -947,11 +952,13 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
                  : variant == QB_VARIANT_IMM8S       ? 4
                  : variant == QB_VARIANT_IMM8A       ? 5
                  : variant == QB_VARIANT_IMM8AS      ? 6
+                 : variant == QB_VARIANT_IMM8AQ      ? 7
                  : variant == QB_VARIANT_AUTO        ? imm_auto_kind(dev, inst_key, auto_kind)
                                                      : 2;
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit form of the same pass)
   if (imm_kind == 2 && L < BMAX + 2) imm_kind = 1;
-  if (imm8_super(imm_kind) && L < BMAX + 2) imm_kind -= 1;
+  if (imm_kind == 7 && L < BMAX + 3) imm_kind = 6;
+  if (imm_kind >= 3 && imm8_nx(imm_kind) == 1 && L < BMAX + 2) imm_kind -= 1;
   QB_TMARK("geometry");
   // the host seed must be a value some searched state attains: the greedy descent keeps the m_fix fixed bits
   // at `suffix`, so it lies in the searched subspace (coarse and tensor-core kernels, any chunk length);
@@ -960,7 +967,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   pl.m_fix = m_fix;
   pl.suffix = suffix;
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2,
-                        imm_kind < 3 ? 0 : (imm8_super(imm_kind) ? 2 : 1) | (imm8_approx(imm_kind) ? 4 : 0)))
+                        imm_kind < 3 ? 0 : (imm8_nx(imm_kind) + 1) | (imm8_approx(imm_kind) ? 4 : 0)))
     return rc;
   QB_TMARK("quantize");
   if (imm_kind >= 3 && pl.imm8_words.size() != (size_t)imm_nwords_of(imm_kind)) {
@@ -1011,7 +1018,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->module_ms = module_ms;
   out->variant = fieldwalk ? QB_VARIANT_FIELDWALK
                  : tc      ? QB_VARIANT_TC
-                 : imm     ? (imm_kind == 6   ? QB_VARIANT_IMM8AS
+                 : imm     ? (imm_kind == 7   ? QB_VARIANT_IMM8AQ
+                              : imm_kind == 6 ? QB_VARIANT_IMM8AS
                               : imm_kind == 5 ? QB_VARIANT_IMM8A
                               : imm_kind == 4 ? QB_VARIANT_IMM8S
                               : imm_kind == 3 ? QB_VARIANT_IMM8
@@ -1150,7 +1158,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   if (imm && imm_kind >= 3 && P.c8_abort_shift >= 0 && dev->h_pass[1] != 0) {
     // the optimistic byte-packed kernel gave up (too many blocks failed its test): nothing of this run is
     // used; run the next tighter kernel.  The device time spent is charged to the result.
-    const int next = imm_kind == 6 ? 5 : imm_kind == 5 ? 3 : imm_kind == 4 ? 3 : 1;
+    const int next = imm_kind == 7 ? 6 : imm_kind == 6 ? 5 : imm_kind == 5 ? 3 : imm_kind == 4 ? 3 : 1;
     const double spent_kernel = out->kernel_ms;
     const double spent_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     guard.unlock();
@@ -1162,7 +1170,15 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     out->total_ms += spent_total;
     return QB_OK;
   }
-  if (imm && variant == QB_VARIANT_AUTO) imm_set_pref(dev, inst_key, imm_kind);
+  if (imm && variant == QB_VARIANT_AUTO) {
+    // remember the kernel for this instance; a run that completed but re-evaluated more blocks than the give-up
+    // rate allows (short runs end before the flag can rise) hands the next solve to the tighter kernel
+    int pref = imm_kind;
+    if (imm_kind >= 3 && P.c8_abort_shift >= 0 &&
+        dev->h_pass[0] > ((out->states >> BMAX) >> P.c8_abort_shift) + (1ull << 12))
+      pref = imm_kind == 7 ? 6 : imm_kind == 6 ? 5 : imm_kind == 5 ? 3 : 1;
+    imm_set_pref(dev, inst_key, pref);
+  }
   if (!fo.found) {
     if (seed && shard_count > 1 && fo.val == LLONG_MAX) {
       // every block of this shard was certified above the seed value, which some state of another shard
@@ -1789,12 +1805,12 @@ int qb_byte_image(const double* coeffs, int n, int kind, uint32_t* words, double
                   int32_t* rneg, int64_t* slack, int32_t* scale_exp) {
   if (!coeffs || !words || !quantized || !inv_unit || !rneg || !slack || !scale_exp)
     return qb::fail(QB_E_ARG, "null pointer");
-  if (kind < 3 || kind > 6) return qb::fail(QB_E_ARG, "kind must be 3..6 (byte-packed threshold kernels)");
+  if (kind < 3 || kind > 7) return qb::fail(QB_E_ARG, "kind must be 3..7 (byte-packed threshold kernels)");
   if (n <= qb::BMAX || n > QB_MAX_DIM) return qb::fail(QB_E_ARG, "needs BMAX < n <= QB_MAX_DIM");
   qb::Plan pl;
   pl.n = n;
   pl.P = std::make_unique<qb::TableParams>();
-  const int img = (qb::imm8_super(kind) ? 2 : 1) | (qb::imm8_approx(kind) ? 4 : 0);
+  const int img = (qb::imm8_nx(kind) + 1) | (qb::imm8_approx(kind) ? 4 : 0);
   if (int rc = qb::quantize(coeffs, n, qb::BMAX, qb::BMAX, pl, false, false, false, img)) return rc;
   if (pl.imm8_words.size() != (size_t)qb::imm_nwords_of(kind))
     return qb::fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
@@ -1811,7 +1827,7 @@ int qb_byte_image(const double* coeffs, int n, int kind, uint32_t* words, double
 
 int qb_imm_image(int kind, int L, const uint32_t* words, unsigned char* out, uint64_t cap, uint64_t* size) {
   if (!words || !size) return qb::fail(QB_E_ARG, "null pointer");
-  if (kind < 1 || kind > 6) return qb::fail(QB_E_ARG, "kind must be 1..6 (see qubrute_b200.h)");
+  if (kind < 1 || kind > 7) return qb::fail(QB_E_ARG, "kind must be 1..7 (see qubrute_b200.h)");
   const qb_imm_cubin* cb = nullptr;
   for (const qb_imm_cubin* c = qb_imm_cubins; c->data; ++c)
     if (c->L == L && c->kind == kind) cb = c;

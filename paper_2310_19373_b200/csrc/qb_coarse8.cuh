@@ -44,9 +44,6 @@
 #ifndef QB_IMM8_LAZY
 #define QB_IMM8_LAZY 9  // of the 16 registers of a row, those whose A_u + table add is one IADD3 (ALU pipe); measured n=40: 8: 25.4, 9: 22.7, 10: 23.2, 11: 23.1, 12: 24.2 ms
 #endif
-#ifndef QB_IMM8A_ALU
-#define QB_IMM8A_ALU 4  // row-bound form: of the 16 adds of a row, those issued as IADD3 on the ALU pipe (the rest: IMAD)
-#endif
 #ifndef QB_IMM8_ABORT_ALLOWANCE
 #define QB_IMM8_ABORT_ALLOWANCE (1ull << 14)  // exact re-evaluations allowed before the optimistic run may give up
 #endif
@@ -71,34 +68,34 @@ __device__ __forceinline__ int coarse8_limit(long long d, float inv_unit) {
   return __float2int_rd(fmaf((float)d, inv_unit, 0.0009765625f));
 }
 
-// AND of the bytes f(z) of a block (four per register); see the file header.  SUPER: the rows also run
-// over one more bit (the first outer bit, field hcx = rint(F_B 2^-s8)): 32 rows, the first 16 of the Gray
-// walk are the block with that bit 0 (out[0]), the last 16 the block with it 1 (out[1]).
+// AND of the bytes f(z) of a block (four per register); see the file header.  NX > 0 (super-blocks): the
+// rows also run over the first NX outer bits (fields FX[t] = F_{B+t}): 16 << NX rows, and out[part] collects
+// the rows of the 10-bit block whose bits B.. have the value `part`.
 //
-// APPROX (QB_VARIANT_IMM8A / IMM8AS, the "row-bound" form): every row uses the SAME row term, the least one,
-// amin = sum_{i in u bits} min(hc_i, 0) <= A_u, folded into the base.  A state's byte is then a lower bound
-// of its coarse value (low by A_u - amin >= 0), so the test stays certified -- a block with no byte under the
-// limit still holds no state under it -- but passes more blocks to the exact evaluation.  In exchange a row
-// costs one 2-input add per register (either integer pipe) instead of a 3-input IADD3 or two IMADs, and
-// the per-row A_u chain disappears.  Pays when the row fields are small against the spread of block
-// minima (sparse instances such as config E); AUTO decides from the instance (qb_api.cu).
-template <int CB1, int CB2, bool SUPER, bool APPROX = false>
-__device__ __forceinline__ void coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2], float FB, int base,
-                                                  unsigned (&out)[2]) {
-  constexpr int B = CB1 + CB2, UB = CB1 + (SUPER ? 1 : 0), NU = 1 << UB, NQ = 1 << (CB2 - 2);
-  static_assert(CB2 >= 3 && CB1 >= 1 && UB <= 5, "four w states per register, at least two registers per row");
+// APPROX (QB_VARIANT_IMM8A / IMM8AS / IMM8AQ, the "row-bound" form): every row uses the SAME row term, the least
+// one, amin = sum_{i in row bits} min(hc_i, 0) <= A_u, folded into the base.  A state's byte is then a lower
+// bound of its coarse value (low by A_u - amin >= 0), so the test stays certified -- a block with no byte
+// under the limit still holds no state under it -- but passes more blocks to the exact evaluation.  In
+// exchange a row costs one 2-input add per register instead of a 3-input IADD3 or two IMADs, and the
+// per-row A_u chain disappears.  The adds are written plainly: ptxas issues about a fifth of them as IADD3
+// (ALU pipe) and the rest as VIADD, which measured faster than any explicit IMAD / IADD3 split (n=40 super-
+// blocks: 15.0 ms against 15.9 ms for 12 IMAD + 4 IADD3 per row, 16.9 / 17.2 / 17.6 ms for 3 / 5 / 6 IADD3).
+template <int CB1, int CB2, int NX, bool APPROX = false>
+__device__ __forceinline__ void coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2],
+                                                  const float (&FX)[NX > 0 ? NX : 1], int base,
+                                                  unsigned (&out)[1 << NX]) {
+  constexpr int B = CB1 + CB2, UB = CB1 + NX, NU = 1 << UB, NQ = 1 << (CB2 - 2), NP = 1 << NX;
+  static_assert(CB2 >= 3 && CB1 >= 1 && UB <= 6, "four w states per register, at least two registers per row");
+  static_assert(APPROX || NX <= 1, "two extra row bits are built for the row-bound form only");
   int hc[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) hc[i] = __float2int_rn(H[i] * p.c8_scale);
-  const unsigned one = p.imm_one;
   if constexpr (APPROX) {
     int amin = 0;
 #pragma unroll
     for (int i = 0; i < CB1; ++i) amin += min(hc[CB2 + i], 0);
-    if constexpr (SUPER) amin += min(__float2int_rn(FB * p.c8_scale), 0);
-    // 0, opaque to ptxas and re-derived per row (else the compiler hoists X4[q] + zero out of the row loop and
-    // issues 2-input VIADDs, which run on the FMA-heavy pipe): makes the ALU-pipe adds 3-input IADD3s
-    const unsigned zero = (unsigned)p.c8_zero;
+#pragma unroll
+    for (int t = 0; t < NX; ++t) amin += min(__float2int_rn(FX[t] * p.c8_scale), 0);
     // X4[q] byte j = base + amin + sum_{i in w} hc_i, w = 4q + j
     unsigned X4[NQ];
     X4[0] = (unsigned)(base + amin) * 0x01010101u + (unsigned)hc[0] * 0x01000100u + (unsigned)hc[1] * 0x01010000u;
@@ -108,25 +105,24 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
 #pragma unroll
       for (int m = 0; m < (1 << (i - 2)); ++m) X4[m + (1 << (i - 2))] = X4[m] + d;
     }
-    unsigned acc[2][2] = {{0xffffffffu, 0xffffffffu}, {0xffffffffu, 0xffffffffu}};
+    unsigned acc[NP][2];
+#pragma unroll
+    for (int h = 0; h < NP; ++h) acc[h][0] = acc[h][1] = 0xffffffffu;
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-      const int half = SUPER ? (u >> CB1) : 0;
+      const int part = u >> CB1;
       const unsigned ph = QB_IMM_PH | (unsigned)(u * NQ);
-      const unsigned zrow = zero & (0x9E3779B9u * (unsigned)(u + 1));  // 0, a different expression per row
       unsigned r[NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const bool alu = ((q + 1) * QB_IMM8A_ALU) / NQ > (q * QB_IMM8A_ALU) / NQ;
-        r[q] = alu ? X4[q] + zrow + (ph | (unsigned)q) : add_fma_pipe(X4[q], one, ph | q);
-      }
+      for (int q = 0; q < NQ; ++q) r[q] = X4[q] + (ph | (unsigned)q);
 #pragma unroll
-      for (int q = 0; q < NQ; q += 2) acc[half][(q >> 1) & 1] &= r[q] & r[q + 1];
+      for (int q = 0; q < NQ; q += 2) acc[part][(q >> 1) & 1] &= r[q] & r[q + 1];
     }
-    out[0] = acc[0][0] & acc[0][1];
-    out[1] = acc[1][0] & acc[1][1];
+#pragma unroll
+    for (int h = 0; h < NP; ++h) out[h] = acc[h][0] & acc[h][1];
     return;
   }
+  const unsigned one = p.imm_one;
   // X4[q] byte j = base + sum_{i in w} hc_i, w = 4q + j
   unsigned X4[NQ];
   X4[0] = (unsigned)base * 0x01010101u + (unsigned)hc[0] * 0x01000100u + (unsigned)hc[1] * 0x01010000u;
@@ -139,13 +135,13 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
   unsigned du[UB];
 #pragma unroll
   for (int i = 0; i < CB1; ++i) du[i] = (unsigned)hc[CB2 + i] * 0x01010101u;
-  if constexpr (SUPER) du[CB1] = (unsigned)__float2int_rn(FB * p.c8_scale) * 0x01010101u;
+  if constexpr (NX > 0) du[CB1] = (unsigned)__float2int_rn(FX[0] * p.c8_scale) * 0x01010101u;
   unsigned a4 = 0u;
   unsigned acc[2][2] = {{0xffffffffu, 0xffffffffu}, {0xffffffffu, 0xffffffffu}};
 #pragma unroll
   for (int g = 0; g < NU; ++g) {
     const int u = g ^ (g >> 1);
-    const int half = SUPER ? (g >> CB1) : 0;  // reflected Gray order: the top row bit is 0 for the first half
+    const int half = NX > 0 ? (g >> CB1) : 0;  // reflected Gray order: the top row bit is 0 for the first half
     if (g) {
       const int i = (g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4;  // ctz(g), g < 32
       a4 = ((u >> i) & 1) ? a4 + du[i] : a4 - du[i];
@@ -163,7 +159,7 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
     for (int q = 0; q < NQ; q += 2) acc[half][(q >> 1) & 1] &= r[q] & r[q + 1];
   }
   out[0] = acc[0][0] & acc[0][1];
-  out[1] = acc[1][0] & acc[1][1];
+  if constexpr (NX > 0) out[1] = acc[1][0] & acc[1][1];
 }
 
 template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false>
@@ -226,8 +222,9 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
       // the block's limit in coarse units relative to its base; no limit yet: everything passes
       const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
       const int lc = min(max(lrel, lc_min), -1);
-      unsigned a[2];
-      coarse8_block_and<CB1, CB2, false, APPROX>(p, H, 0.f, 127 - lc, a);
+      unsigned a[1];
+      const float nofx[1] = {0.f};
+      coarse8_block_and<CB1, CB2, 0, APPROX>(p, H, nofx, 127 - lc, a);
       if (lrel < 0 && (a[0] & 0x80808080u) == 0x80808080u) continue;  // no state of the block is under the limit
       ++npass;
       const long long val = V + (long long)block_min<B1, B2, 0, NF>(p, H, F);
@@ -249,24 +246,25 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
 }
 
-// Super-block form (QB_VARIANT_IMM8S): the byte image also covers the first outer bit B, as in
-// coarse2_kernel (qb_coarse2.cuh): one pass tests the two blocks that differ only in bit B against the
-// same limit (relative to the base V of the half with bit B = 0), the outer Gray walk runs over bits
-// B+1 .. L-1, and each half that holds a byte under the limit is re-evaluated exactly from its own base,
-// in original block order j = 2 j' + (b ^ (j' & 1)), so keys, records and finalize_kernel see the
-// blocks of the 10-bit walk.  Certified bound: (11 + 1)/2 coarse units.
-template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false>
+// Super-block forms (QB_VARIANT_IMM8S / IMM8AS: NX = 1; IMM8AQ: NX = 2): the byte image also covers the first NX
+// outer bits B .. B+NX-1, as in coarse2_kernel (qb_coarse2.cuh): one pass tests the 2^NX blocks that differ only
+// in those bits against the same limit (relative to the base V of the block with those bits 0), the outer
+// Gray walk runs over bits B+NX .. L-1, and each block that holds a byte under the limit is re-evaluated
+// exactly from its own base, in original block order j = (j' << NX) + t: block j has bits B.. equal to the low
+// NX bits of the reflected Gray code of j, so keys, records and finalize_kernel see the blocks of the 10-bit
+// walk.  Certified bound: (10 + NX + 1)/2 coarse units (in c8_slack).
+template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false, int NX = 1>
 __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(CB1 + CB2 == B && B == BMAX, "super-blocks extend the 10-bit table blocks");
-  static_assert(L >= B + 2, "needs at least one walked outer bit besides bit B");
-  constexpr int LO = L - B;   // outer bits of the 10-bit walk (block index j has LO bits)
-  constexpr int LS = LO - 1;  // walked bits B+1 .. L-1 (super-block index j')
+  static_assert(NX >= 1 && NX <= 2 && L >= B + NX + 1, "needs at least one walked outer bit besides the image bits");
+  constexpr int LO = L - B;    // outer bits of the 10-bit walk (block index j has LO bits)
+  constexpr int LS = LO - NX;  // walked bits B+NX .. L-1 (super-block index j')
   constexpr int NF = LO;
   Rec best{LLONG_MAX, ~0ull, 0ull, 0u, 0u};
   const unsigned long long nchunks = p.chunk_end - p.chunk_begin;
   const int lane = threadIdx.x & 31;
-  const long long slack = p.c8_slack + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);  // (11+1)/2 coarse units
+  const long long slack = p.c8_slack + (p.mode == MODE_SEARCH_RECORD ? p.theta_add : 0ll);
   const float inv_unit = p.c8_scale;
   const int lc_min = -p.c8_rneg - 1;
 
@@ -309,28 +307,50 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
       if (jp) {
         const int r = __ffs(jp) - 1;
         const float sg = ((jp >> (r + 1)) & 1u) ? -1.f : 1.f;
-        outer_flip<B, L, B + 1>(p, B + 1 + r, sg, V, H, F);
+        outer_flip<B, L, B + NX>(p, B + NX + r, sg, V, H, F);
       }
       if (LS <= 5 || (jp & 31u) == 0u) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
       const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
       const int lc = min(max(lrel, lc_min), -1);
-      unsigned a[2];
-      coarse8_block_and<CB1, CB2, true, APPROX>(p, H, F[0], 127 - lc, a);
-      if (lrel < 0 && (a[0] & a[1] & 0x80808080u) == 0x80808080u) continue;  // neither half holds a state under the limit
+      unsigned a[1 << NX];
+      float FX[NX];
+#pragma unroll
+      for (int t = 0; t < NX; ++t) FX[t] = F[t];
+      coarse8_block_and<CB1, CB2, NX, APPROX>(p, H, FX, 127 - lc, a);
+      unsigned all = a[0];
+#pragma unroll
+      for (int h = 1; h < (1 << NX); ++h) all &= a[h];
+      if (lrel < 0 && (all & 0x80808080u) == 0x80808080u) continue;  // no block holds a state under the limit
 #pragma unroll 1
-      for (int t = 0; t < 2; ++t) {
-        const int b = t ^ (int)(jp & 1u);  // half evaluated in original block order j = 2 jp + t
-        if (lrel < 0 && ((b ? a[1] : a[0]) & 0x80808080u) == 0x80808080u) continue;
+      for (int t = 0; t < (1 << NX); ++t) {
+        // block j = (jp << NX) + t of the 10-bit walk: its bits B.. are the low NX bits of gray(j)
+        const unsigned int j = (jp << NX) + (unsigned)t;
+        const int part = (int)((j ^ (j >> 1)) & ((1u << NX) - 1u));
+        unsigned ap = a[0];
+#pragma unroll
+        for (int h = 1; h < (1 << NX); ++h) ap = (part == h) ? a[h] : ap;
+        if (lrel < 0 && (ap & 0x80808080u) == 0x80808080u) continue;
         ++npass;
-        // exact fp32 table evaluation from the half's own base: (V, H) or (V + q_BB + F_B, H + q_.B)
+        // exact fp32 table evaluation from the block's own base
         float Hb[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) Hb[i] = b ? H[i] + p.Qs[B][i] : H[i];
-        const long long Vb = b ? V + (long long)(p.d[B] + F[0]) : V;
-        const long long val = Vb + (long long)block_min<B1, B2, 0, NF>(p, Hb, F);
+        for (int i = 0; i < B; ++i) {
+          float h = H[i];
+#pragma unroll
+          for (int e = 0; e < NX; ++e) h += ((part >> e) & 1) ? p.Qs[B + e][i] : 0.f;
+          Hb[i] = h;
+        }
+        float dv = 0.f;
+#pragma unroll
+        for (int e = 0; e < NX; ++e) {
+          if (!((part >> e) & 1)) continue;
+          dv += p.d[B + e] + F[e];
+#pragma unroll
+          for (int e2 = e + 1; e2 < NX; ++e2) dv += ((part >> e2) & 1) ? p.Qs[B + e][B + e2] : 0.f;
+        }
+        const long long val = V + (long long)dv + (long long)block_min<B1, B2, 0, NF>(p, Hb, F);
         cmin = min(cmin, val);
         if (val <= best.val) {
-          const unsigned int j = 2u * jp + (unsigned)t;
           const unsigned long long K = block_key(p, key_hi, dir, j, LO);
           if (val < best.val || K < best.K) best = Rec{val, K, c, j, 0u};
           if (val < thr) {

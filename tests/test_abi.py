@@ -157,9 +157,9 @@ def test_imm_cubin_patches_every_placeholder(kind, L, tmp_path):
     assert sum(int(w) in imms for w in words) >= nw - 20
 
 
-@pytest.mark.parametrize("kind,L", [(3, 10), (3, 20), (4, 12), (4, 20), (5, 10), (5, 12), (5, 20), (6, 14), (6, 20), (6, 22)])
+@pytest.mark.parametrize("kind,L", [(3, 10), (3, 20), (4, 12), (4, 20), (5, 10), (5, 12), (5, 20), (6, 14), (6, 20), (6, 22), (7, 13), (7, 20)])
 def test_byte_kernel_cubin_patches_every_placeholder(kind, L):
-    """QB_VARIANT_IMM8 / IMM8S / IMM8A / IMM8AS (kinds 3..6): every placeholder of the embedded cubin is
+    """QB_VARIANT_IMM8 / IMM8S / IMM8A / IMM8AS (kinds 3..7): every placeholder of the embedded cubin is
     replaced by the instance's packed byte word (IMAD / IADD3 / UIADD3 immediates) and none survives.
     Host only."""
     import struct
@@ -170,8 +170,9 @@ def test_byte_kernel_cubin_patches_every_placeholder(kind, L):
     words[(words >> 16) == 0x7A5C] = 1  # keep the test words distinguishable from placeholders
     img = _lib.imm_image(L, words, kind)
     (name, off, size), = list(_text_sections(img))
-    fam = "coarse8s_kernel" if kind in (4, 6) else "coarse8_kernel"
-    assert f"{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}E" in name
+    nx = {4: 1, 6: 1, 7: 2}.get(kind, 0)
+    fam = "coarse8s_kernel" if nx else "coarse8_kernel"
+    assert f"{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}E" + (f"Li{nx}E" if nx else "") in name
     found = set()
     want = set(int(w) for w in words)
     for at in range(off, off + size, 16):

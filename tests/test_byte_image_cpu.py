@@ -1,7 +1,7 @@
 """CPU replay of the byte-packed threshold test (qb_coarse8.cuh) on the image the library builds.
 
-qb_byte_image (host only) returns what the threshold kernels of kind 3..6 (QB_VARIANT_IMM8, IMM8S, IMM8A,
-IMM8AS) would run an instance with: the packed table words, the quantized instance, fl(1/unit), Rneg and the
+qb_byte_image (host only) returns what the threshold kernels of kind 3..7 (QB_VARIANT_IMM8, IMM8S, IMM8A,
+IMM8AS, IMM8AQ) would run an instance with: the packed table words, the quantized instance, fl(1/unit), Rneg and the
 certified slack.  This test recomputes, in numpy and with the device's float operations, the bytes
 f(z) = base + sum hc_i z_i + Tc8(z) of randomly chosen blocks and checks the two claims the kernel's
 correctness rests on:
@@ -45,8 +45,8 @@ def _subset_sums(vals):
 def _replay(c, kind, rng, nblocks=120):
     words, q, inv, rneg, slack, _e = _lib.byte_image(c, kind)
     n = q.shape[0]
-    sup, approx = kind in (4, 6), kind in (5, 6)
-    nb = B + 1 if sup else B
+    approx = kind in (5, 6, 7)
+    nb = B + {4: 1, 6: 1, 7: 2}.get(kind, 0)
     tc8 = _decode_words(words)
     assert len(tc8) == 1 << nb and np.abs(tc8).max() <= 127
     qs = q + np.triu(q, 1).T  # symmetric, diagonal once
@@ -85,14 +85,14 @@ def _replay(c, kind, rng, nblocks=120):
 CASES = [("E", 40, 0), ("E", 33, 3), ("D", 32, 0), ("D", 36, 1), ("B", 34, 2), ("A", 36, 5)]
 
 
-@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+@pytest.mark.parametrize("kind", [3, 4, 5, 6, 7])
 @pytest.mark.parametrize("name,n,rep", CASES)
 def test_byte_image_range_and_no_false_negatives(name, n, rep, kind):
     c = instances.config_coeffs(name, rep, n=n)
     assert _replay(c, kind, np.random.default_rng(1000 * kind + n)) == 0
 
 
-@pytest.mark.parametrize("kind", [3, 4, 5, 6])
+@pytest.mark.parametrize("kind", [3, 4, 5, 6, 7])
 def test_byte_image_tie_heavy_and_wide_range(kind):
     rng = np.random.default_rng(kind)
     assert _replay(instances.int_uniform_coeffs(33, 777, -1, 1), kind, rng) == 0

@@ -177,7 +177,7 @@ def test_config_e_n40_properties():
     inst = qb.QuboInstance(c)
     sol = qb.solve_incremental(inst)
     auto = _lib.solve(c)
-    assert auto.variant in (_lib.VARIANT_IMM, _lib.VARIANT_IMM2)  # n=40: a patched-immediate coarse kernel
+    assert auto.variant in _lib.IMM_VARIANTS  # n=40: a patched-immediate coarse kernel
     table = _lib.solve(c, variant=_lib.VARIANT_TABLE)
     coarse = _lib.solve(c, variant=_lib.VARIANT_COARSE)
     for other in (table, coarse):
@@ -558,7 +558,7 @@ def test_n40_other_instance_types(name):
     a = _lib.solve(c)
     b = _lib.solve(c, variant=_lib.VARIANT_TABLE)
     d = _lib.solve(c, variant=_lib.VARIANT_COARSE)
-    assert a.variant in (_lib.VARIANT_IMM, _lib.VARIANT_IMM2)
+    assert a.variant in _lib.IMM_VARIANTS
     assert b.variant == _lib.VARIANT_TABLE and d.variant == _lib.VARIANT_COARSE
     assert (a.argmin_bits, a.value, a.tie_key) == (b.argmin_bits, b.value, b.tie_key)
     assert (a.argmin_bits, a.value, a.tie_key) == (d.argmin_bits, d.value, d.tie_key)

@@ -1,0 +1,12 @@
+#!/bin/bash
+# r13: full GPU suite on the byte-packed kernels + AUTO policy, bench line, ncu capture of AUTO's n=40 kernel
+cd "$(dirname "$0")/.."
+timeout 900 python tools/auto_probe.py 2>&1 | tee gpurun_out/auto_probe2.log
+timeout 2400 python -m pytest tests -q -m gpu -rs --timeout 1500 > gpurun_out/pytest_gpu_r13i.log 2>&1; echo "pytest rc $?"
+grep -E "passed|failed|^FAILED|^ERROR|SKIPPED" gpurun_out/pytest_gpu_r13i.log | tail -15
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r13i.log 2>&1; echo "smoke rc $?"; tail -2 gpurun_out/smoke_r13i.log
+timeout 300 python tools/profile_case.py E 40 0 && \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k "regex:coarse8s_kernel" -s 1 -c 1 -o gpurun_out/r13_ncu_imm8as_E python tools/profile_case.py E 40 0 > gpurun_out/ncu_imm8as.log 2>&1; echo "ncu rc $?"
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r13i.json 2> gpurun_out/bench_r13i.err; echo "bench rc $?"
+cat gpurun_out/bench_r13i.json | head -c 1500

@@ -78,6 +78,8 @@ if record:
         sym, sha = imm_symbol(int(targs[2]), 2), imm_sass_sha256(int(targs[2]), 2)
     elif fam in ("coarse8_kernel", "coarse8s_kernel"):  # byte-packed threshold kernels (embedded cubins)
         kind = (4 if fam == "coarse8s_kernel" else 3) + (2 if targs[6] in ("true", "1") else 0)
+        if fam == "coarse8s_kernel" and len(targs) > 7 and targs[7] == "2":
+            kind = 7
         sym, sha = imm_symbol(int(targs[4]), kind), imm_sass_sha256(int(targs[4]), kind)
     else:
         sym = kernel_symbol(lib_path, fam, int(targs[4]))
