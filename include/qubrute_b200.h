@@ -56,9 +56,10 @@ extern "C" {
 #define QB_VARIANT_IMM8S 8     /* the same over 11-bit super-blocks (chunks of >= 12 free bits) */
 #define QB_VARIANT_IMM8A 9     /* row-bound form of IMM8: every row of a block is tested with the least row term
                                   (a certified lower bound of each state), one 2-input add per four states */
-#define QB_VARIANT_IMM8AS 10   /* row-bound form of IMM8S */
+#define QB_VARIANT_IMM8AS 10   /* row-bound form of IMM8S; AUTO's first choice where the coarse filter runs (it gives
+                                  up and re-runs with IMM8A / IMM8 / IMM when too many blocks fail its test) */
 #define QB_VARIANT_IMM8AQ 11   /* row-bound form over 12-bit super-blocks (four blocks per pass, chunks of >= 13
-                                  free bits); AUTO's first choice where the coarse filter runs */
+                                  free bits); measured no faster than IMM8AS, kept as an option */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {

@@ -399,7 +399,7 @@ static bool imm_enabled() {
 }
 
 #ifndef QB_IMM_AUTO_KIND
-#define QB_IMM_AUTO_KIND 7  // AUTO's patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3 ms), 3 = byte-packed threshold pass (22.7 ms), 4 = its super-blocks (21.7 ms)
+#define QB_IMM_AUTO_KIND 6  // AUTO's first patched-immediate kernel (n=40): 1 = 16-bit min pass (29.7 ms), 2 = its 11-bit super-blocks (30.3), 3 / 4 = byte-packed threshold pass / super-blocks (23.6 / 21.0), 5 / 6 = their row-bound forms (18.1 / 15.5), 7 = row-bound 12-bit super-blocks (15.8; 25 ms on dense int instances)
 #endif
 #ifndef QB_IMM8_ABORT_SHIFT
 #define QB_IMM8_ABORT_SHIFT 10  // AUTO: a byte-packed kernel gives up beyond 1 exact re-evaluation per 2^10 blocks (~ +10% time)
