@@ -79,7 +79,8 @@ __device__ __forceinline__ int coarse8_limit(long long d, float inv_unit) {
 // exchange a row costs one 2-input add per register instead of a 3-input IADD3 or two IMADs, and the
 // per-row A_u chain disappears.  The adds are written plainly: ptxas issues about a fifth of them as IADD3
 // (ALU pipe) and the rest as VIADD, which measured faster than any explicit IMAD / IADD3 split (n=40 super-
-// blocks: 15.0 ms against 15.9 ms for 12 IMAD + 4 IADD3 per row, 16.9 / 17.2 / 17.6 ms for 3 / 5 / 6 IADD3).
+// blocks: 15.5 ms against 15.9 ms for 12 IMAD + 4 IADD3 per row, 16.9 / 17.2 / 17.6 ms for 3 / 5 / 6 IADD3; forcing
+// one or two more IADD3 per row on top of ptxas's split: 15.9 / 15.8 ms).
 template <int CB1, int CB2, int NX, bool APPROX = false>
 __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2],
                                                   const float (&FX)[NX > 0 ? NX : 1], int base,
