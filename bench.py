@@ -108,7 +108,7 @@ def imm_sass_sha256(L: int, kind: int = 1):
 def imm_symbol(L: int, kind: int = 1) -> str:
     if kind >= 3:  # byte-packed threshold kernels: 3 + super-block + 2 * row-bound form; 7: row-bound, 12-bit blocks
         nx = {4: 1, 6: 1, 7: 2}.get(kind, 0)
-        fam, tail = ("15coarse8s_kernel", f"Li{nx}E") if nx else ("14coarse8_kernel", "")
+        fam, tail = ("15coarse8s_kernel", f"Li{nx}ELb0E") if nx else ("14coarse8_kernel", "")
         return f"_ZN2qb{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}E{tail}EEvNS_11TableParamsE"
     if kind == 2:
         return f"_ZN2qb14coarse2_kernelILi5ELi5ELi{L}ELi128EEEvNS_11TableParamsE"
@@ -151,7 +151,7 @@ def fp32_lane_peak_per_sm_clk():
 FAMILIES = {1: "table_kernel", 2: "fieldwalk_kernel", 3: "coarse_kernel", 4: "tc_kernel", 5: "coarse_kernel (imm)",
             6: "coarse2_kernel (imm)", 7: "coarse8_kernel (imm)", 8: "coarse8s_kernel (imm)",
             9: "coarse8_kernel (imm, row-bound)", 10: "coarse8s_kernel (imm, row-bound)",
-            11: "coarse8s_kernel (imm, row-bound, 12-bit)"}
+            11: "coarse8s_kernel (imm, row-bound, 12-bit)", 12: "coarse8s_kernel"}
 
 
 def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path):
@@ -164,7 +164,7 @@ def roofline_block(r, n, per_launch_states, search_s, sm_count, sm_hz, lib_path)
     state's value with ~1 instruction instead of n+1 additions."""
     L = n - int(r.prefix_bits)
     family = FAMILIES.get(int(r.variant))
-    if int(r.variant) >= 5:  # patched-immediate kernels: SASS of the embedded cubin, placeholders in place
+    if 5 <= int(r.variant) <= 11:  # patched-immediate kernels: SASS of the embedded cubin, placeholders in place
         kind = int(r.variant) - 4
         sym, sha = imm_symbol(L, kind), imm_sass_sha256(L, kind)
     else:
@@ -562,12 +562,13 @@ def main():
         # kernel and the literal per-step field walk (QB_VARIANT_COARSE / _TABLE / _FIELDWALK)
         names = {0: "auto", 1: "table", 2: "fieldwalk", 3: "coarse_tableload", 4: "tc", 5: "coarse_imm",
                  6: "coarse_imm_superblock", 7: "threshold_imm8", 8: "threshold_imm8_superblock", 9: "threshold_imm8_rowbound",
-                 10: "threshold_imm8_rowbound_superblock", 11: "threshold_imm8_rowbound_12bit"}
+                 10: "threshold_imm8_rowbound_superblock", 11: "threshold_imm8_rowbound_12bit",
+                 12: "threshold_byte8_tableload"}
         line["variants"] = {f"{names[int(r.variant)]} (default)": {
             "search_ms": search_s * 1e3, "states_per_s": per_launch_states / search_s}}
         # (the tensor-core pass, QB_VARIANT_TC, is retired from this list: 40 ms, TMEM round-trip bound,
         # DESIGN.md section 4)
-        for var in (_lib.VARIANT_IMM8AQ, _lib.VARIANT_IMM8AS, _lib.VARIANT_IMM8A, _lib.VARIANT_IMM8S, _lib.VARIANT_IMM8, _lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE,
+        for var in (_lib.VARIANT_BYTE8, _lib.VARIANT_IMM8AQ, _lib.VARIANT_IMM8AS, _lib.VARIANT_IMM8A, _lib.VARIANT_IMM8S, _lib.VARIANT_IMM8, _lib.VARIANT_IMM, _lib.VARIANT_COARSE, _lib.VARIANT_TABLE,
                     _lib.VARIANT_FIELDWALK):
             _lib.solve(inst.coeffs, variant=var)
             vr = _lib.solve(inst.coeffs, variant=var)

@@ -60,6 +60,9 @@ extern "C" {
                                   up and re-runs with IMM8A / IMM8 / IMM when too many blocks fail its test) */
 #define QB_VARIANT_IMM8AQ 11   /* row-bound form over 12-bit super-blocks (four blocks per pass, chunks of >= 13
                                   free bits); measured no faster than IMM8AS, kept as an option */
+#define QB_VARIANT_BYTE8 12    /* IMM8AS with its table words read from the kernel parameters instead of patched
+                                  immediates: no module load (AUTO's first solve of an instance), chunks of >= 12
+                                  free bits */
 
 /* Result of one solve (or of one shard of a sharded solve). */
 typedef struct qb_result {

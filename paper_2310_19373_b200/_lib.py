@@ -20,7 +20,8 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("QB_LIB_PATH") or os.path.join(PKG_DIR, "libqubrute_b200.so")
 HEADER = os.path.join(REPO_DIR, "include", "qubrute_b200.h")
 SOURCES = [os.path.join(PKG_DIR, "csrc", f)
-           for f in ("qb_api.cu", "qb_k_table.cu", "qb_k_coarse.cu", "qb_k_fieldwalk.cu", "qb_k_batch.cu", "qb_k_tc.cu")]
+           for f in ("qb_api.cu", "qb_k_table.cu", "qb_k_coarse.cu", "qb_k_fieldwalk.cu", "qb_k_batch.cu", "qb_k_tc.cu",
+                     "qb_k_byte8.cu")]
 DEPS = [os.path.join(PKG_DIR, "csrc", f) for f in os.listdir(os.path.join(PKG_DIR, "csrc"))] + [HEADER]
 # patched-immediate coarse kernels (QB_VARIANT_IMM): one cubin per chunk length, embedded in the .so
 IMM_SOURCE = os.path.join(PKG_DIR, "csrc", "qb_k_coarse_imm.cu")
@@ -55,9 +56,11 @@ VARIANT_IMM8S = 8
 VARIANT_IMM8A = 9
 VARIANT_IMM8AS = 10
 VARIANT_IMM8AQ = 11
-# the patched-immediate search kernels (AUTO picks among them where the coarse filter runs)
+VARIANT_BYTE8 = 12
+# the search kernels AUTO picks among where the coarse filter runs, besides the table-load COARSE: the
+# patched-immediate kernels and the table-load byte kernel
 IMM_VARIANTS = (VARIANT_IMM, VARIANT_IMM2, VARIANT_IMM8, VARIANT_IMM8S, VARIANT_IMM8A, VARIANT_IMM8AS,
-                VARIANT_IMM8AQ)
+                VARIANT_IMM8AQ, VARIANT_BYTE8)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -59,20 +59,23 @@ struct KernelSet {
   KFn coarse = nullptr;     // packed-int16 filter search kernel with the same blocks (big geometry only)
   KFn coarse_fin = nullptr; // its one-CTA record reduction (the coarse kernel only writes records)
   KFn tc = nullptr;         // tensor-core coarse pass (records only; reduced by coarse_fin)
+  KFn byte8 = nullptr;      // table-load byte-packed threshold pass (records only; reduced by coarse_fin)
   std::atomic<int> occ{-1};     // resident CTAs per SM for `search` (lazy; shared by all devices)
   std::atomic<int> occ_fw{-1};  // ... for `fieldwalk`
   std::atomic<int> occ_c{-1};   // ... for `coarse`
   std::atomic<int> occ_t{-1};   // ... for `tc`
+  std::atomic<int> occ_b{-1};   // ... for `byte8`
 };
 
 static std::vector<std::unique_ptr<KernelSet>>& kernel_sets() {
   static std::vector<std::unique_ptr<KernelSet>> sets = [] {
     std::vector<std::unique_ptr<KernelSet>> v;
-    int nt = 0, nc = 0, nf = 0, ntc = 0;
+    int nt = 0, nc = 0, nf = 0, ntc = 0, nb8 = 0;
     const TableFns* t = table_fns(&nt);
     const LFn* c = coarse_fns(&nc);
     const LFn* f = fieldwalk_fns(&nf);
     const LFn* tcf = tc_fns(&ntc);
+    const LFn* b8 = byte8_fns(&nb8);
     for (int i = 0; i < nt; ++i) {
       auto k = std::make_unique<KernelSet>();
       k->B1 = t[i].B1; k->B2 = t[i].B2; k->L = t[i].L;
@@ -86,6 +89,8 @@ static std::vector<std::unique_ptr<KernelSet>>& kernel_sets() {
           }
         for (int j = 0; j < nf; ++j)
           if (f[j].L == k->L) k->fieldwalk = f[j].fn;
+        for (int j = 0; j < nb8; ++j)
+          if (b8[j].L == k->L) k->byte8 = b8[j].fn;
         for (int j = 0; j < ntc; ++j)
           if (tcf[j].L == k->L) {
             k->tc = tcf[j].fn;
@@ -314,11 +319,11 @@ static bool imm_patch(std::vector<unsigned char>& img, const unsigned* words, in
 static int imm8_nx(int kind) { return kind == 7 ? 2 : (kind == 4 || kind == 6) ? 1 : 0; }
 static bool imm8_approx(int kind) { return kind >= 5 && kind <= 7; }
 static std::string imm_kernel_name(int kind, int L) {
-  if (kind >= 3)  // 3..7: coarse8_kernel<..., APPROX> / coarse8s_kernel<..., APPROX, NX>
+  if (kind >= 3)  // 3..7: coarse8_kernel<..., APPROX> / coarse8s_kernel<..., APPROX, NX, TABLE = false>
     return std::string(imm8_nx(kind) ? "_ZN2qb15coarse8s_kernelILi" : "_ZN2qb14coarse8_kernelILi") +
            std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" + std::to_string(QB_COARSE_B1) + "ELi" +
            std::to_string(QB_COARSE_B2) + "ELi" + std::to_string(L) + "ELi" + std::to_string(TPB) + "ELb" +
-           (imm8_approx(kind) ? "1" : "0") + "E" + (imm8_nx(kind) ? "Li" + std::to_string(imm8_nx(kind)) + "E" : "") +
+           (imm8_approx(kind) ? "1" : "0") + "E" + (imm8_nx(kind) ? "Li" + std::to_string(imm8_nx(kind)) + "ELb0E" : "") +
            "EEvNS_11TableParamsE";
   if (kind == 2)
     return "_ZN2qb14coarse2_kernelILi" + std::to_string(BIG_B1) + "ELi" + std::to_string(BIG_B2) + "ELi" +
@@ -909,7 +914,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     return fail(QB_E_ARG, "fixed_bits must be in [" + std::to_string(m_fix) + ", " + std::to_string(n) + ")");
   if (rule == RULE_INTEGER) m_tie = m_fix;
   if (shard_count == 0 || shard >= shard_count) return fail(QB_E_ARG, "shard index out of range");
-  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_IMM8AQ) return fail(QB_E_ARG, "unknown variant");
+  if (variant < QB_VARIANT_AUTO || variant > QB_VARIANT_BYTE8) return fail(QB_E_ARG, "unknown variant");
 
   Device* dev = nullptr;
   if (int rc = get_device(&dev)) return rc;
@@ -942,9 +947,20 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   // the coarse pass with the instance's table as instruction immediates (AUTO: whenever the coarse kernel
   // runs, unless QB_IMM=0); QB_VARIANT_COARSE forces the table-load coarse kernel.  Kind 2 = the 11-bit
   // super-block kernel (needs L >= B + 2), AUTO's kind unless QB_IMM_KIND=1.
-  bool imm = coarse && (variant >= QB_VARIANT_IMM || (variant == QB_VARIANT_AUTO && imm_enabled()));
+  bool imm = coarse && ((variant >= QB_VARIANT_IMM && variant != QB_VARIANT_BYTE8) ||
+                        (variant == QB_VARIANT_AUTO && imm_enabled()));
   // AUTO: the instance's identity for the module / preference caches (the tables depend on coeffs and L only)
   const unsigned long long inst_key = (imm && variant == QB_VARIANT_AUTO) ? instance_key(coeffs, n, L) : 0ull;
+  // AUTO takes a patched module when the search is long or the instance was solved before (imm_auto); else,
+  // and for QB_VARIANT_BYTE8, the table-load byte kernel runs (no module to load; auto_kind < 0: a retry
+  // after it gave up, which takes the 16-bit table-load kernel)
+  if (imm && variant == QB_VARIANT_AUTO && auto_kind == 0) {
+    const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 3.0e13 * 1e3;
+    imm = imm_auto(dev, L, inst_key, est_ms);
+  }
+  if (auto_kind < 0) imm = false;
+  bool byte8 = coarse && !imm && pl.ks->byte8 != nullptr &&
+               (variant == QB_VARIANT_BYTE8 || (variant == QB_VARIANT_AUTO && imm_enabled() && auto_kind >= 0));
   // (super-blocks need chunks of >= B + 2 free bits; shorter chunks take the 10-bit kernel, reported as IMM)
   int imm_kind = !imm                                ? 0
                  : variant == QB_VARIANT_IMM         ? 1
@@ -967,9 +983,21 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   pl.m_fix = m_fix;
   pl.suffix = suffix;
   if (int rc = quantize(coeffs, n, fieldwalk ? L : BE, pl.B, pl, tc, seed, imm_kind == 2,
-                        imm_kind < 3 ? 0 : (imm8_nx(imm_kind) + 1) | (imm8_approx(imm_kind) ? 4 : 0)))
+                        byte8          ? (2 | 4)  // the row-bound 11-bit image
+                        : imm_kind < 3 ? 0
+                                       : (imm8_nx(imm_kind) + 1) | (imm8_approx(imm_kind) ? 4 : 0)))
     return rc;
   QB_TMARK("quantize");
+  if (byte8) {
+    if (pl.imm8_words.size() == (size_t)kImm8sWords) {
+      std::memcpy(pl.P->Tc8w, pl.imm8_words.data(), sizeof(pl.P->Tc8w));
+      if (variant == QB_VARIANT_AUTO) pl.P->c8_abort_shift = QB_IMM8_ABORT_SHIFT;
+    } else if (variant == QB_VARIANT_BYTE8) {
+      return fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
+    } else {
+      byte8 = false;
+    }
+  }
   if (imm_kind >= 3 && pl.imm8_words.size() != (size_t)imm_nwords_of(imm_kind)) {
     // no shift makes the block's coarse range fit a byte (cannot happen for finite coefficients, kept as a guard)
     if (variant != QB_VARIANT_AUTO) return fail(QB_E_INTERNAL, "no byte-packed coarse image for this instance");
@@ -995,13 +1023,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
 
   std::memset(out, 0, sizeof(*out));
   cudaKernel_t imm_fn = nullptr;
-  if (imm && variant == QB_VARIANT_AUTO) {
-    const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 3.0e13 * 1e3;
-    imm = imm_auto(dev, L, inst_key, est_ms);
-    // AUTO runs the byte-packed kernels optimistically: one that has to re-evaluate more than 1 block in 2^10
-    // exactly gives up and the solve is re-run with the next tighter kernel (6 -> 5 -> 3 -> 1), see below
-    if (imm && imm_kind >= 3) P.c8_abort_shift = QB_IMM8_ABORT_SHIFT;
-  }
+  // AUTO runs the byte-packed kernels optimistically: one that has to re-evaluate more than 1 block in 2^10
+  // exactly gives up and the solve is re-run with the next tighter kernel (6 -> 5 -> 3 -> 1), see below
+  if (imm && variant == QB_VARIANT_AUTO && imm_kind >= 3) P.c8_abort_shift = QB_IMM8_ABORT_SHIFT;
   double module_ms = 0.0;
   if (imm) {
     bool loaded = false;
@@ -1018,6 +1042,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   out->module_ms = module_ms;
   out->variant = fieldwalk ? QB_VARIANT_FIELDWALK
                  : tc      ? QB_VARIANT_TC
+                 : byte8   ? QB_VARIANT_BYTE8
                  : imm     ? (imm_kind == 7   ? QB_VARIANT_IMM8AQ
                               : imm_kind == 6 ? QB_VARIANT_IMM8AS
                               : imm_kind == 5 ? QB_VARIANT_IMM8A
@@ -1040,8 +1065,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
 
   KernelSet& ks = *pl.ks;
-  const KFn search_fn = fieldwalk ? ks.fieldwalk : tc ? ks.tc : (coarse ? ks.coarse : ks.search);
-  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : tc ? ks.occ_t : (coarse ? ks.occ_c : ks.occ);
+  const KFn search_fn = fieldwalk ? ks.fieldwalk : tc ? ks.tc : byte8 ? ks.byte8 : (coarse ? ks.coarse : ks.search);
+  std::atomic<int>& occ_cache = fieldwalk ? ks.occ_fw : tc ? ks.occ_t : byte8 ? ks.occ_b : (coarse ? ks.occ_c : ks.occ);
   // (the patched-immediate kernel: same registers / launch bounds as the coarse kernel -> its occupancy)
   const int tpb = tc ? TC_TPB : TPB, smem = tc ? TC_SMEM : 0, rows = tc ? TC_WORKERS : TPB;
   int occ = occ_cache.load();
@@ -1104,7 +1129,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   }
   out->launches = 1;
   out->grid = grid;
-  if (imm || search_fn == ks.coarse || search_fn == ks.tc) {
+  if (imm || search_fn == ks.coarse || search_fn == ks.tc || search_fn == ks.byte8) {
     ks.coarse_fin<<<1, TPB, 0, st>>>(P);
     QB_CUDA(cudaGetLastError());
     out->launches = 2;
@@ -1135,7 +1160,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   // one readback: the search result, and on the collect path the counts plus the first candidates
   QB_CUDA(cudaMemcpyAsync(dev->h_final, dev->d_final, sizeof(FinalOut), cudaMemcpyDeviceToHost, st));
   dev->h_pass[0] = dev->h_pass[1] = 0;
-  if (imm_kind >= 3)
+  if (imm_kind >= 3 || byte8)
     QB_CUDA(cudaMemcpyAsync(dev->h_pass, dev->d_work + 6, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   if (collect) {
     QB_CUDA(cudaMemcpyAsync(dev->h_counts, dev->d_counts, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1155,10 +1180,13 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   const FinalOut fo = *dev->h_final;
   out->exact_blocks = dev->h_pass[0];
   out->retries = retries;
-  if (imm && imm_kind >= 3 && P.c8_abort_shift >= 0 && dev->h_pass[1] != 0) {
+  if (((imm && imm_kind >= 3) || byte8) && P.c8_abort_shift >= 0 && dev->h_pass[1] != 0) {
     // the optimistic byte-packed kernel gave up (too many blocks failed its test): nothing of this run is
     // used; run the next tighter kernel.  The device time spent is charged to the result.
-    const int next = imm_kind == 7 ? 6 : imm_kind == 6 ? 5 : imm_kind == 5 ? 3 : imm_kind == 4 ? 3 : 1;
+    // (the table-load byte kernel hands over to the 16-bit table-load kernel, and the instance's next solve --
+    // a patched module -- starts from the next tighter form)
+    const int next = byte8 ? -1 : imm_kind == 7 ? 6 : imm_kind == 6 ? 5 : imm_kind == 5 ? 3 : imm_kind == 4 ? 3 : 1;
+    if (byte8) imm_set_pref(dev, inst_key, 5);
     const double spent_kernel = out->kernel_ms;
     const double spent_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     guard.unlock();
@@ -1170,6 +1198,9 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
     out->total_ms += spent_total;
     return QB_OK;
   }
+  if (byte8 && variant == QB_VARIANT_AUTO &&
+      dev->h_pass[0] > ((out->states >> BMAX) >> P.c8_abort_shift) + (1ull << 12))
+    imm_set_pref(dev, inst_key, 5);  // too many exact re-evaluations for the row-bound 11-bit form
   if (imm && variant == QB_VARIANT_AUTO) {
     // remember the kernel for this instance; a run that completed but re-evaluated more blocks than the give-up
     // rate allows (short runs end before the flag can rise) hands the next solve to the tighter kernel

@@ -81,13 +81,16 @@ __device__ __forceinline__ int coarse8_limit(long long d, float inv_unit) {
 // (ALU pipe) and the rest as VIADD, which measured faster than any explicit IMAD / IADD3 split (n=40 super-
 // blocks: 15.5 ms against 15.9 ms for 12 IMAD + 4 IADD3 per row, 16.9 / 17.2 / 17.6 ms for 3 / 5 / 6 IADD3; forcing
 // one or two more IADD3 per row on top of ptxas's split: 15.9 / 15.8 ms).
-template <int CB1, int CB2, int NX, bool APPROX = false>
+// TABLE: the packed table words come from the kernel parameters (p.Tc8w, LDCU.128 into uniform registers, one load
+// per 16 states) instead of patched immediates: no module to patch and load, about 14% more instructions.
+template <int CB1, int CB2, int NX, bool APPROX = false, bool TABLE = false>
 __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const float (&H)[CB1 + CB2],
                                                   const float (&FX)[NX > 0 ? NX : 1], int base,
                                                   unsigned (&out)[1 << NX]) {
   constexpr int B = CB1 + CB2, UB = CB1 + NX, NU = 1 << UB, NQ = 1 << (CB2 - 2), NP = 1 << NX;
   static_assert(CB2 >= 3 && CB1 >= 1 && UB <= 6, "four w states per register, at least two registers per row");
   static_assert(APPROX || NX <= 1, "two extra row bits are built for the row-bound form only");
+  static_assert(!TABLE || (APPROX && NX == 1), "the table-load form exists for the row-bound 11-bit pass");
   int hc[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) hc[i] = __float2int_rn(H[i] * p.c8_scale);
@@ -115,7 +118,7 @@ __device__ __forceinline__ void coarse8_block_and(const TableParams& p, const fl
       const unsigned ph = QB_IMM_PH | (unsigned)(u * NQ);
       unsigned r[NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) r[q] = X4[q] + (ph | (unsigned)q);
+      for (int q = 0; q < NQ; ++q) r[q] = X4[q] + (TABLE ? p.Tc8w[u * NQ + q] : (ph | (unsigned)q));
 #pragma unroll
       for (int q = 0; q < NQ; q += 2) acc[part][(q >> 1) & 1] &= r[q] & r[q + 1];
     }
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
 // exactly from its own base, in original block order j = (j' << NX) + t: block j has bits B.. equal to the low
 // NX bits of the reflected Gray code of j, so keys, records and finalize_kernel see the blocks of the 10-bit
 // walk.  Certified bound: (10 + NX + 1)/2 coarse units (in c8_slack).
-template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false, int NX = 1>
+template <int B1, int B2, int CB1, int CB2, int L, int TPB, bool APPROX = false, int NX = 1, bool TABLE = false>
 __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __grid_constant__ TableParams p) {
   constexpr int B = B1 + B2;
   static_assert(CB1 + CB2 == B && B == BMAX, "super-blocks extend the 10-bit table blocks");
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
       float FX[NX];
 #pragma unroll
       for (int t = 0; t < NX; ++t) FX[t] = F[t];
-      coarse8_block_and<CB1, CB2, NX, APPROX>(p, H, FX, 127 - lc, a);
+      coarse8_block_and<CB1, CB2, NX, APPROX, TABLE>(p, H, FX, 127 - lc, a);
       unsigned all = a[0];
 #pragma unroll
       for (int h = 1; h < (1 << NX); ++h) all &= a[h];

@@ -115,6 +115,9 @@ struct alignas(16) TableParams {
   int c8_zero;
   int c8_abort_shift;
   long long c8_slack;
+  // the same byte image as kernel-parameter words (row-bound 11-bit form, word z >> 2): the table-load
+  // byte kernel (QB_VARIANT_BYTE8) reads them through uniform registers instead of patched immediates
+  unsigned Tc8w[1 << (BMAX - 1)];
 };
 
 enum { RULE_GRAY = 0, RULE_INTEGER = 1 };

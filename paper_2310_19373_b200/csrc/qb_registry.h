@@ -46,6 +46,7 @@ const TableFns* table_fns(int* count);    // qb_k_table.cu
 const LFn* coarse_fns(int* count);        // qb_k_coarse.cu
 const LFn* fieldwalk_fns(int* count);     // qb_k_fieldwalk.cu
 const LFn* tc_fns(int* count);            // qb_k_tc.cu (tensor-core coarse pass; null fin = finalize_kernel)
+const LFn* byte8_fns(int* count);         // qb_k_byte8.cu (table-load byte-packed threshold pass)
 const BatchFn* batch_fns(int* count);     // qb_k_batch.cu: index = block bits B (1..BMAX)
 BatchFn batch_warp_fn(int* warps, int* nmin, int* nmax);  // qb_k_batch.cu: one warp per instance
 

@@ -172,7 +172,10 @@ def test_byte_kernel_cubin_patches_every_placeholder(kind, L):
     (name, off, size), = list(_text_sections(img))
     nx = {4: 1, 6: 1, 7: 2}.get(kind, 0)
     fam = "coarse8s_kernel" if nx else "coarse8_kernel"
-    assert f"{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}E" + (f"Li{nx}E" if nx else "") in name
+    assert f"{fam}ILi5ELi5ELi4ELi6ELi{L}ELi128ELb{int(kind >= 5)}E" + (f"Li{nx}ELb0E" if nx else "") in name
+    import bench
+
+    assert name == ".text." + bench.imm_symbol(L, kind)  # the symbol bench.py hashes is the one in the cubin
     found = set()
     want = set(int(w) for w in words)
     for at in range(off, off + size, 16):

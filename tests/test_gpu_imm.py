@@ -78,18 +78,22 @@ def test_imm_vs_oracle_subspace_n34(var):
     c = instances.config_coeffs("E", 7, n=34)
     m, suffix = 8, 77
     got = _lib.solve(c, m, suffix, m, variant=var)
-    assert got.variant in IMMS
+    # (the table-load byte kernel exists for chunks of >= 12 free bits; this geometry has shorter ones and
+    # QB_VARIANT_BYTE8 then runs the 16-bit table-load kernel)
+    assert got.variant in IMMS or (var == _lib.VARIANT_BYTE8 and got.variant == _lib.VARIANT_COARSE)
     bits, val, _ = O.solve_subspaces(c, m, suffix, suffix + 1, threads=8)
     assert int(got.argmin_bits) == bits and got.value == val
 
 
 def test_auto_policy_first_solve_and_repeat():
-    """AUTO takes the patched kernel on a first solve only when the search is long (n=40), and on
-    the repeat of a table it has seen (n=33); a first n=33 solve stays on the table-load kernel."""
+    """AUTO takes a patched kernel on a first solve only when the search is long (n=40), and on
+    the repeat of an instance it has seen (n=33); a first n=33 solve runs a table-load kernel (the byte
+    kernel, no module to load)."""
     c33 = instances.config_coeffs("E", 41, n=33)
     first = _lib.solve(c33)
     again = _lib.solve(c33)
-    assert first.variant == _lib.VARIANT_COARSE and again.variant in IMMS
+    assert first.variant == _lib.VARIANT_BYTE8 and int(first.module_ms * 1e6) == 0
+    assert again.variant in IMMS and again.variant != _lib.VARIANT_BYTE8
     assert _same(first, again)
     c40 = instances.config_coeffs("E", 42, n=40)
     assert _lib.solve(c40).variant in IMMS
@@ -125,3 +129,25 @@ def test_imm2_tie_heavy_against_oracle_full():
         else:
             bits, val, _ = O.solve_subspaces(c, m_tie, threads=8)
         assert int(got.argmin_bits) == bits and got.value == val
+
+
+@pytest.mark.parametrize("scale", [1.0, 0.37])
+def test_auto_gives_up_on_a_dense_instance_and_retries(scale):
+    """AUTO's optimistic run: on dense integers in +-1000 at n=36 the row-bound byte kernels re-evaluate far
+    more than 1 block in 2^10, so the run gives up and the solve is repeated with a tighter kernel
+    (qb_result.retries); the answer is the table-load kernel's either way, on the exact path (scale 1) and on
+    the certified collect path (non-integer coefficients, scale 0.37)."""
+    c = instances.config_coeffs("D", 0, n=36) * scale
+    ref = _lib.solve(c, variant=_lib.VARIANT_COARSE)
+    first = _lib.solve(c)            # first solve of a short instance: a table-load kernel (the byte kernel gives up)
+    runs = [_lib.solve(c) for _ in range(3)]
+    assert first.variant in (_lib.VARIANT_COARSE, _lib.VARIANT_BYTE8) and int(first.retries) >= 1
+    for r in [first] + runs:
+        assert _same(r, ref)
+    assert all(r.variant in _lib.IMM_VARIANTS for r in runs)
+    # the kind that completed is remembered: the last solve starts from it and does not retry
+    assert int(runs[-1].retries) == 0 and runs[-1].variant != _lib.VARIANT_IMM8AS
+    # an explicit variant never gives up
+    forced = _lib.solve(c, variant=_lib.VARIANT_IMM8AS)
+    assert forced.variant == _lib.VARIANT_IMM8AS and int(forced.retries) == 0 and _same(forced, ref)
+    assert int(forced.exact_blocks) > (2 ** 26 >> 10)

@@ -13,7 +13,7 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 for n in ns:
     c = instances.config_coeffs(name, 0, n=n)
     out = {}
-    for var, label in ((_lib.VARIANT_IMM, "imm"), (_lib.VARIANT_IMM8, "imm8"), (_lib.VARIANT_IMM8S, "imm8s"), (_lib.VARIANT_IMM8A, "imm8a"), (_lib.VARIANT_IMM8AS, "imm8as"), (_lib.VARIANT_IMM8AQ, "imm8aq")):
+    for var, label in ((_lib.VARIANT_IMM, "imm"), (_lib.VARIANT_IMM8, "imm8"), (_lib.VARIANT_IMM8S, "imm8s"), (_lib.VARIANT_IMM8A, "imm8a"), (_lib.VARIANT_IMM8AS, "imm8as"), (_lib.VARIANT_IMM8AQ, "imm8aq"), (_lib.VARIANT_BYTE8, "byte8")):
         _lib.solve(c, variant=var)
         rs = [_lib.solve(c, variant=var) for _ in range(reps)]
         r = rs[-1]

@@ -76,7 +76,8 @@ if record:
         sym, sha = imm_symbol(int(targs[4])), imm_sass_sha256(int(targs[4]))
     elif fam == "coarse2_kernel":  # super-block patched-immediate kernel (embedded cubin)
         sym, sha = imm_symbol(int(targs[2]), 2), imm_sass_sha256(int(targs[2]), 2)
-    elif fam in ("coarse8_kernel", "coarse8s_kernel"):  # byte-packed threshold kernels (embedded cubins)
+    elif fam in ("coarse8_kernel", "coarse8s_kernel") and not (len(targs) > 8 and targs[8] in ("true", "1")):
+        # byte-packed threshold kernels with patched immediates (embedded cubins)
         kind = (4 if fam == "coarse8s_kernel" else 3) + (2 if targs[6] in ("true", "1") else 0)
         if fam == "coarse8s_kernel" and len(targs) > 7 and targs[7] == "2":
             kind = 7
