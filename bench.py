@@ -544,6 +544,8 @@ def main():
         "config": bench_config(args.config, n),
         "geometry": {"shards": world, "parallelism": f"prefix-shard x{world}", "prefix_bits": int(r.prefix_bits),
                      "exact_path": bool(r.exact), "scale_exp": int(r.scale_exp), "candidates": int(r.candidates),
+                     "exact_blocks": int(r.exact_blocks), "blocks": int(per_launch_states) >> 10,
+                     "auto_retries": int(r.retries),
                      "argmin": hex(qb.bits_to_int(sol.minimizer)), "min_value": sol.value},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": int(r.param_bytes) * int(r.launches),

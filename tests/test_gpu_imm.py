@@ -151,3 +151,20 @@ def test_auto_gives_up_on_a_dense_instance_and_retries(scale):
     forced = _lib.solve(c, variant=_lib.VARIANT_IMM8AS)
     assert forced.variant == _lib.VARIANT_IMM8AS and int(forced.retries) == 0 and _same(forced, ref)
     assert int(forced.exact_blocks) > (2 ** 26 >> 10)
+
+
+def test_all_minimisers_through_the_byte_kernels(monkeypatch):
+    """Every minimiser of a tie-heavy n=32 instance (values in {-1, 0, 1}): the recording search of the
+    byte-packed kernels (first solve: table-load form; repeats: patched forms) lists exactly the states the
+    16-bit table-load kernel lists (QB_IMM=0), in the same tie order, each with the minimum value."""
+    c = instances.int_uniform_coeffs(32, 4242, -1, 1)
+    monkeypatch.setenv("QB_IMM", "0")
+    v0, xs0, n0 = _lib.all_minimisers(c)
+    monkeypatch.delenv("QB_IMM")
+    assert n0 >= 1 and len(xs0) == n0
+    for _ in range(3):
+        v, xs, cnt = _lib.all_minimisers(c)
+        assert (v, cnt) == (v0, n0) and np.array_equal(xs, xs0)
+    for x in xs0[:8]:
+        bits = np.array([(int(x) >> i) & 1 for i in range(32)], dtype=np.float64)
+        assert _lib.eval_upper(c, bits) == v0
