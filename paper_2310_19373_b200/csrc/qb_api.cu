@@ -341,9 +341,10 @@ static unsigned long long imm_hash(int kind, int L, const unsigned* words, int n
   return h;
 }
 
-// AUTO's choice: patching + loading a module costs ~1-3 ms of host time, so a first solve only takes
-// the patched-immediate kernel when its search is long (>= QB_IMM_MIN_MS, default 16 ms of estimated
-// search); a table already loaded, or one solved before on this device, always does.
+// AUTO's choice: patching + loading a module costs about 1 ms of host time and the patched kernel is 8%
+// faster than the table-load byte kernel, so a first solve only takes it when its search is long
+// (>= QB_IMM_MIN_MS, default 12 ms of estimated search at 7e13 states/s: n >= 40 on one GPU); an instance
+// already loaded, or one solved before on this device, always does.
 static bool imm_auto(Device* dev, int L, unsigned long long h, double est_ms) {
   for (auto& m : dev->imm)
     if (m.lib && m.L == L && m.inst == h) return true;
@@ -351,7 +352,7 @@ static bool imm_auto(Device* dev, int L, unsigned long long h, double est_ms) {
   for (unsigned long long x : dev->imm_seen) seen |= (x == h);
   if (!seen) dev->imm_seen[dev->imm_seen_next++ % kImmSeen] = h;
   const char* e = std::getenv("QB_IMM_MIN_MS");
-  const double min_ms = e ? std::atof(e) : 16.0;
+  const double min_ms = e ? std::atof(e) : 12.0;
   return seen || est_ms >= min_ms;
 }
 
@@ -955,7 +956,7 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
   // and for QB_VARIANT_BYTE8, the table-load byte kernel runs (no module to load; auto_kind < 0: a retry
   // after it gave up, which takes the 16-bit table-load kernel)
   if (imm && variant == QB_VARIANT_AUTO && auto_kind == 0) {
-    const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 3.0e13 * 1e3;
+    const double est_ms = std::ldexp(1.0, n - m_fix) / (double)shard_count / 7.0e13 * 1e3;
     imm = imm_auto(dev, L, inst_key, est_ms);
   }
   if (auto_kind < 0) imm = false;
