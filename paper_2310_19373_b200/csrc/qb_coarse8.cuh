@@ -45,7 +45,7 @@
 #define QB_IMM8_LAZY 9  // of the 16 registers of a row, those whose A_u + table add is one IADD3 (ALU pipe); measured n=40: 8: 25.4, 9: 22.7, 10: 23.2, 11: 23.1, 12: 24.2 ms
 #endif
 #ifndef QB_IMM8_ABORT_ALLOWANCE
-#define QB_IMM8_ABORT_ALLOWANCE (1ull << 14)  // exact re-evaluations allowed before the optimistic run may give up
+#define QB_IMM8_ABORT_ALLOWANCE (1ull << 16)  // exact re-evaluations allowed before the optimistic run may give up (start-up transient)
 #endif
 #ifndef QB_IMM8_MINB
 #define QB_IMM8_MINB 4
@@ -66,6 +66,22 @@ __device__ __forceinline__ unsigned add_fma_reg(unsigned a, unsigned one, unsign
 // 2^-10 before the floor never under-estimates it; over-estimating only passes more blocks.
 __device__ __forceinline__ int coarse8_limit(long long d, float inv_unit) {
   return __float2int_rd(fmaf((float)d, inv_unit, 0.0009765625f));
+}
+
+// AUTO's optimistic run (p.c8_abort_shift >= 0), checked every 64 blocks of a long chunk: the thread adds the
+// blocks it re-evaluated exactly since its last report to the device-wide count work[6] and gives up
+// (work[7] = 1) when that count exceeds the allowed rate -- 1 in 2^shift of the blocks walked so far, estimated
+// as this thread's own progress times the resident threads -- plus a start-up allowance.
+__device__ __forceinline__ bool coarse8_give_up(const TableParams& p, unsigned& npass, unsigned long long my_blocks,
+                                                unsigned long long nthreads) {
+  if (p.c8_abort_shift < 0) return false;
+  if (npass) {
+    atomicAdd(p.work + 6, (unsigned long long)npass);
+    npass = 0;
+  }
+  if (__ldcg(p.work + 6) <= ((my_blocks * nthreads) >> p.c8_abort_shift) + QB_IMM8_ABORT_ALLOWANCE) return false;
+  p.work[7] = 1ull;
+  return true;
 }
 
 // AND of the bytes f(z) of a block (four per register); see the file header.  NX > 0 (super-blocks): the
@@ -180,7 +196,11 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
   const float inv_unit = p.c8_scale;
   const int lc_min = -p.c8_rneg - 1;
 
+  bool quit = false;
+  unsigned long long my_chunks = 0;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * TPB;
   for (;;) {
+    if (__any_sync(0xffffffffu, quit)) break;  // a lane gave up inside its chunk (below): the whole warp stops
     unsigned long long base = 0, passed = 0;
     if (lane == 0) {
       base = atomicAdd(p.work, 32ull);
@@ -222,7 +242,13 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
         outer_flip<B, L, B>(p, B + r, sg, V, H, F);
       }
       // device-wide best: refreshed every block in short chunks, every 64 blocks in long ones
-      if (LO <= 6 || (j & 63u) == 0u) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+      if (LO <= 6 || (j & 63u) == 0u) {
+        thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+        if (LO > 6 && coarse8_give_up(p, npass, (my_chunks << LO) + j, nthreads)) {
+          quit = true;
+          break;
+        }
+      }
       // the block's limit in coarse units relative to its base; no limit yet: everything passes
       const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
       const int lc = min(max(lrel, lc_min), -1);
@@ -244,6 +270,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8_kernel(const __grid
     }
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
     if (npass) atomicAdd(p.work + 6, (unsigned long long)npass);
+    ++my_chunks;
   }
   // records only: the reduction runs as finalize_kernel (qb_table.cuh)
   const Rec r = cta_reduce<TPB>(best);
@@ -272,7 +299,11 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
   const float inv_unit = p.c8_scale;
   const int lc_min = -p.c8_rneg - 1;
 
+  bool quit = false;
+  unsigned long long my_chunks = 0;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * TPB;
   for (;;) {
+    if (__any_sync(0xffffffffu, quit)) break;  // a lane gave up inside its chunk (below): the whole warp stops
     unsigned long long base = 0, passed = 0;
     if (lane == 0) {
       base = atomicAdd(p.work, 32ull);
@@ -313,7 +344,13 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
         const float sg = ((jp >> (r + 1)) & 1u) ? -1.f : 1.f;
         outer_flip<B, L, B + NX>(p, B + NX + r, sg, V, H, F);
       }
-      if (LS <= 5 || (jp & 31u) == 0u) thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+      if (LS <= 5 || (jp & 31u) == 0u) {
+        thr = min(thr, gbest_dec(__ldcg(p.gbest)));
+        if (LS > 5 && coarse8_give_up(p, npass, (my_chunks << LO) + ((unsigned long long)jp << NX), nthreads)) {
+          quit = true;
+          break;
+        }
+      }
       const int lrel = thr > LLONG_MAX - slack ? 0 : coarse8_limit(thr + slack - V, inv_unit);
       const int lc = min(max(lrel, lc_min), -1);
       unsigned a[1 << NX];
@@ -366,6 +403,7 @@ __global__ void __launch_bounds__(TPB, QB_IMM8_MINB) coarse8s_kernel(const __gri
     }
     if (p.mode == MODE_SEARCH_RECORD) p.chunk_min[ci] = cmin;
     if (npass) atomicAdd(p.work + 6, (unsigned long long)npass);
+    ++my_chunks;
   }
   const Rec r = cta_reduce<TPB>(best);
   if (threadIdx.x == 0) p.cta_out[blockIdx.x] = r;
