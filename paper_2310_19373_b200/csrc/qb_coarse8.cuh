@@ -1,5 +1,10 @@
-// Byte-packed threshold kernel (QB_VARIANT_IMM8): the patched-immediate coarse pass with FOUR states
-// per 32-bit register.
+// Byte-packed threshold kernels: the coarse pass with FOUR states per 32-bit register.
+//   QB_VARIANT_IMM8 / IMM8S          exact row terms, 10-bit blocks / 11-bit super-blocks (patched immediates)
+//   QB_VARIANT_IMM8A / IMM8AS / AQ   the row-bound form (coarse8_block_and, APPROX), 10 / 11 / 12-bit blocks;
+//                                    IMM8AS is AUTO's search kernel for long or repeated solves
+//   QB_VARIANT_BYTE8                 IMM8AS with its table words in the kernel parameters (qb_k_byte8.cu)
+// AUTO runs them optimistically: coarse8_give_up() stops a run whose blocks fail the test too often, and the
+// host repeats the solve with a tighter kernel (qb_api.cu).
 //
 // Same chunks, outer Gray walk, blocks, tie keys, exact re-evaluation and records as coarse_kernel
 // (qb_coarse.cuh).  What changes is the coarse test of a 1024-state block.  The 16-bit pass forms the

@@ -106,7 +106,8 @@ struct alignas(16) TableParams {
   // byte-packed threshold pass (qb_coarse8.cuh): coarse unit U quantized units (any real U >= 1, not only
   // powers of two), c8_scale = fl(1/U); c8_slack = the certified rounding margin ceil(U ((NB+1)/2 + 0.02)) in
   // quantized units (NB image bits); Rneg = how far below its base a block's tested values can reach (limits
-  // are clamped at -Rneg - 1); c8_zero = 0, opaque to the compiler (ALU-pipe 3-input adds)
+  // are clamped at -Rneg - 1); c8_zero = 0 (an opaque zero for forcing 3-input adds in pipe-split experiments;
+  // no kernel reads it now)
   // c8_abort_shift >= 0: AUTO's optimistic run -- the kernel gives up (work[7] = 1) once the blocks it had
   // to re-evaluate exactly (work[6]) exceed blocks_started >> c8_abort_shift plus a start-up allowance, and the
   // host re-runs the solve with a tighter kernel; negative: never
