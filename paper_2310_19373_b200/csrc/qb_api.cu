@@ -1276,7 +1276,8 @@ static int solve_impl(const double* coeffs, int n, int m_fix, unsigned long long
       P.coeffs64 = dev->d_coeffs;
       P.red = dev->d_red;
       QB_CUDA(cudaMemsetAsync(dev->d_red, 0xff, 2 * sizeof(unsigned long long), st));
-      const int nstates_grid = dev->sms * 2;
+      // the fp64 sums are dependent add chains: latency-bound, so fill the SMs (8 CTAs of 4 warps each)
+      const int nstates_grid = dev->sms * 8;
       P.mode = MODE_REDUCE_VALUE;
       ks.states<<<nstates_grid, 128, 0, st>>>(P);
       QB_CUDA(cudaGetLastError());

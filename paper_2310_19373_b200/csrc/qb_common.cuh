@@ -224,14 +224,18 @@ __device__ __forceinline__ Rec cta_reduce(Rec r, int nwarps = TPB / 32) {
   return r;
 }
 
-// eval_upper (_kernels.py:12-20) on the device: same row-major fp64 order, no FMA contraction
+// eval_upper (_kernels.py:12-20) on the device: same row-major fp64 order, no FMA contraction.  Only the terms
+// with x_i = x_j = 1 are added, in the reference's order: every other product is +-0.0, and adding +-0.0 never
+// changes the running sum (which starts at +0.0 and so is never -0.0), so the result is bit-identical to the
+// full double loop at a quarter of its terms (the overflow reduction evaluates up to 10^9 candidates).
 __device__ __forceinline__ double eval_upper_dev(const double* c, int n, unsigned long long x) {
   double acc = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const double xi = (double)((x >> i) & 1ull);
-    for (int j = i; j < n; ++j) {
-      const double xj = (double)((x >> j) & 1ull);
-      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c[i * n + j], xi), xj));
+  for (unsigned long long xi = x; xi; xi &= xi - 1ull) {
+    const int i = __ffsll((long long)xi) - 1;
+    const double* row = c + (size_t)i * n;
+    for (unsigned long long xj = xi; xj; xj &= xj - 1ull) {  // set bits j >= i, ascending
+      const int j = __ffsll((long long)xj) - 1;
+      acc = __dadd_rn(acc, row[j]);  // c_ij * 1 * 1 = c_ij exactly
     }
   }
   return acc;

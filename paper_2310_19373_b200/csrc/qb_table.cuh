@@ -321,6 +321,11 @@ __global__ void __launch_bounds__(128) collect_states_kernel(const __grid_consta
     const unsigned int j = (unsigned int)(e & 0xffffffffu);
     const unsigned long long s = chunk_prefix(p, p.chunk_begin + ci);
     const unsigned long long xo = (s << L) | ((unsigned long long)(j ^ (j >> 1)) << BE);
+    // overflow path (MODE_REDUCE_*): exact fp64 value of every candidate, lexicographic (value, key) minimum;
+    // each lane keeps its own minimum over the block and the warp issues ONE atomic per block (a massively
+    // tied instance has 10^9 candidates: one atomic each on a single word took seconds)
+    unsigned long long lane_min = ~0ull;
+    const unsigned long long best_vk = (p.mode == MODE_REDUCE_KEY) ? __ldcg(&p.red[0]) : 0ull;
     for_block_states<B, SB, L>(p, xo, lane, 32, [&](unsigned int zb, long long val) {
       if (val > theta) return;
       const unsigned long long x = xo | zb;
@@ -328,12 +333,16 @@ __global__ void __launch_bounds__(128) collect_states_kernel(const __grid_consta
         const unsigned long long idx = atomicAdd(p.cand_count, 1ull);
         if (idx < p.cand_cap) p.cand[idx] = x;
       } else {
-        // overflow path: exact fp64 value of every candidate, lexicographic (value, key) minimum
         const unsigned long long vk = ordered_f64(eval_upper_dev(p.coeffs64, p.n, x));
-        if (p.mode == MODE_REDUCE_VALUE) atomicMin(&p.red[0], vk);
-        else if (vk == p.red[0]) atomicMin(&p.red[1], state_tie_key(x, p.n, p.m_tie, p.rule));
+        if (p.mode == MODE_REDUCE_VALUE) lane_min = min(lane_min, vk);
+        else if (vk == best_vk) lane_min = min(lane_min, state_tie_key(x, p.n, p.m_tie, p.rule));
       }
     });
+    if (p.mode != MODE_COLLECT) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) lane_min = min(lane_min, __shfl_xor_sync(0xffffffffu, lane_min, off));
+      if (lane == 0 && lane_min != ~0ull) atomicMin(&p.red[p.mode == MODE_REDUCE_VALUE ? 0 : 1], lane_min);
+    }
   }
 }
 
