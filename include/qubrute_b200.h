@@ -154,6 +154,12 @@ int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, con
 int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                    double* kernel_ms);
 
+/* The same for a batch held as float (BASELINE config C stores float32 Q): every coefficient is widened to
+ * double exactly, so results are those of qb_solve_batch on the converted array, without the caller first
+ * writing that 2x larger array. */
+int qb_solve_batch_f32(const float* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
+                       double* kernel_ms);
+
 /* The batch sharded over several GPUs of this process: contiguous slices
  * of the instances, slice i solved by qb_solve_batch on devices[i] from its own host thread, results
  * written in place (the gather is the caller's arrays).  *kernel_ms = the maximum over slices.  A

@@ -124,6 +124,8 @@ SIGNATURES = {
     "qb_gray_scan": (ctypes.c_int, [_dp, _dp, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _dp,
                                     _u64p]),
     "qb_solve_batch": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, _u64p, _dp, _dp]),
+    "qb_solve_batch_f32": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int, ctypes.c_uint64, _u64p, _dp,
+                                          _dp]),
     "qb_solve_batch_devices": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int),
                                               ctypes.c_int, _u64p, _dp, _dp]),
     "qb_prefix_eval": (ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _dp, _dp]),
@@ -329,13 +331,20 @@ def gray_scan(coeffs, qua, lin, x0, v0, n_free, device: int | None = None):
 
 
 def solve_batch(coeffs_batch, device: int | None = None):
-    c = _f64(coeffs_batch)
+    """(argmin bits, values, device window ms) of a (count, n, n) batch; a float32 array goes to
+    qb_solve_batch_f32 as it is (no fp64 copy), anything else is converted to fp64."""
+    f32 = isinstance(coeffs_batch, np.ndarray) and coeffs_batch.dtype == np.float32
+    c = np.ascontiguousarray(coeffs_batch) if f32 else _f64(coeffs_batch)
     count, n = c.shape[0], c.shape[1]
     init(device)
     bits = np.zeros(count, dtype=np.uint64)
     vals = np.zeros(count)
     ms = ctypes.c_double()
-    rc = lib().qb_solve_batch(_ptr(c), n, count, bits.ctypes.data_as(_u64p), _ptr(vals), ctypes.byref(ms))
+    if f32:
+        rc = lib().qb_solve_batch_f32(c.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n, count,
+                                      bits.ctypes.data_as(_u64p), _ptr(vals), ctypes.byref(ms))
+    else:
+        rc = lib().qb_solve_batch(_ptr(c), n, count, bits.ctypes.data_as(_u64p), _ptr(vals), ctypes.byref(ms))
     check(rc, "qb_solve_batch")
     return bits, vals, ms.value
 

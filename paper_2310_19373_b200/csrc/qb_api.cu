@@ -1384,7 +1384,10 @@ static int prefix_impl(const double* coeffs, int n, int k, uint64_t c_begin, uin
 // contraction), as fp32 when every folded value round-trips exactly, else as fp64.  Host threads
 // (OpenMP) split the instances.  Returns the format written, or -1 with *bad = the lowest instance
 // holding a non-finite coefficient.
-static int pack_batch_piece(const double* coeffs, int n, uint64_t b0, uint64_t b1, void* out, uint64_t* bad) {
+// T: the caller's element type (double, or float for qb_solve_batch_f32: folded in fp64 exactly like the
+// converted array would be, without the caller first widening 4 MB to 8 MB)
+template <class T>
+static int pack_batch_piece(const T* coeffs, int n, uint64_t b0, uint64_t b1, void* out, uint64_t* bad) {
   const int ntri = n * (n + 1) / 2;
   const long long cnt = (long long)(b1 - b0);
   long long first_bad = LLONG_MAX;
@@ -1392,13 +1395,13 @@ static int pack_batch_piece(const double* coeffs, int n, uint64_t b0, uint64_t b
   float* o32 = static_cast<float*>(out);
 #pragma omp parallel for schedule(static) reduction(min : first_bad) reduction(| : not_f32) if (cnt >= 256)
   for (long long t = 0; t < cnt; ++t) {
-    const double* c = coeffs + (b0 + t) * (uint64_t)n * n;
+    const T* c = coeffs + (b0 + t) * (uint64_t)n * n;
     float* o = o32 + t * ntri;
     int p = 0;
     for (int i = 0; i < n; ++i) {
-      const double* row = c + (size_t)i * n;
+      const T* row = c + (size_t)i * n;
       for (int j = i; j < n; ++j, ++p) {
-        const double v = (j == i) ? row[i] : row[j] + c[(size_t)j * n + i];
+        const double v = (j == i) ? (double)row[i] : (double)row[j] + (double)c[(size_t)j * n + i];
         if (!std::isfinite(row[j]) || !std::isfinite(c[(size_t)j * n + i])) first_bad = std::min(first_bad, (long long)(b0 + t));
         const float f = (float)v;
         not_f32 |= ((double)f != v);
@@ -1414,16 +1417,18 @@ static int pack_batch_piece(const double* coeffs, int n, uint64_t b0, uint64_t b
   double* o64 = static_cast<double*>(out);
 #pragma omp parallel for schedule(static) if (cnt >= 256)
   for (long long t = 0; t < cnt; ++t) {
-    const double* c = coeffs + (b0 + t) * (uint64_t)n * n;
+    const T* c = coeffs + (b0 + t) * (uint64_t)n * n;
     double* o = o64 + t * ntri;
     int p = 0;
     for (int i = 0; i < n; ++i)
-      for (int j = i; j < n; ++j, ++p) o[p] = (j == i) ? c[(size_t)i * n + i] : c[(size_t)i * n + j] + c[(size_t)j * n + i];
+      for (int j = i; j < n; ++j, ++p)
+        o[p] = (j == i) ? (double)c[(size_t)i * n + i] : (double)c[(size_t)i * n + j] + (double)c[(size_t)j * n + i];
   }
   return BATCH_UPPER_F64;
 }
 
-static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
+template <class T>
+static int batch_impl(const T* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                       double* kernel_ms) {
   if (!coeffs || !argmin_bits || !values) return fail(QB_E_ARG, "null pointer");
   if (n < 1) return fail(QB_E_ARG, "dimension must be at least 1");
@@ -1528,10 +1533,10 @@ static int batch_impl(const double* coeffs, int n, uint64_t count, uint64_t* arg
   // instances with more than BATCH_CAP near-tied minimisers: full single-instance path
   std::vector<double> up((size_t)n * n);
   for (uint64_t b : fallback) {
-    const double* c = coeffs + b * (uint64_t)n * n;
+    const T* c = coeffs + b * (uint64_t)n * n;
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j)
-        up[(size_t)i * n + j] = j < i ? 0.0 : (j == i ? c[i * n + i] : c[i * n + j] + c[j * n + i]);
+        up[(size_t)i * n + j] = j < i ? 0.0 : (j == i ? (double)c[i * n + i] : (double)c[i * n + j] + (double)c[j * n + i]);
     qb_result r;
     if (int rc = solve_impl(up.data(), n, 0, 0, 0, RULE_GRAY, 0, 1, QB_VARIANT_AUTO, &r)) return rc;
     argmin_bits[b] = r.argmin_bits;
@@ -1795,6 +1800,11 @@ int qb_gray_scan(const double* coeffs, const double* qua, const double* lin, con
 
 int qb_solve_batch(const double* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
                    double* kernel_ms) {
+  return qb::batch_impl(coeffs, n, count, argmin_bits, values, kernel_ms);
+}
+
+int qb_solve_batch_f32(const float* coeffs, int n, uint64_t count, uint64_t* argmin_bits, double* values,
+                       double* kernel_ms) {
   return qb::batch_impl(coeffs, n, count, argmin_bits, values, kernel_ms);
 }
 

@@ -198,7 +198,8 @@ def _batch_coeffs(instances) -> np.ndarray:
     """(count, n, n) fp64 upper-triangular coefficients, normalised like QuboInstance
     (lower triangle folded, finiteness and cap checked), vectorised over the batch."""
     if isinstance(instances, np.ndarray):
-        arr = np.asarray(instances, dtype=np.float64)
+        # a float32 batch stays float32: the native path widens each coefficient exactly (qb_solve_batch_f32)
+        arr = instances if instances.dtype == np.float32 else np.asarray(instances, dtype=np.float64)
         if arr.ndim != 3 or arr.shape[1] != arr.shape[2]:
             raise ValueError(f"batch must have shape (count, n, n), got {arr.shape}")
         n = arr.shape[1]

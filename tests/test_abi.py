@@ -14,7 +14,7 @@ from paper_2310_19373_b200 import _lib
 
 def _declared_symbols():
     text = open(_lib.HEADER).read()
-    return sorted(set(re.findall(r"\b(qb_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(qb_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_and_binding_agree():

@@ -160,3 +160,27 @@ def test_solve_devices_nccl_combine(monkeypatch):
     r2 = _lib.solve_devices(c, [0, 0])
     assert r2.combine == 0
     assert (r2.argmin_bits, r2.value, r2.tie_key) == (whole.argmin_bits, whole.value, whole.tie_key)
+
+
+@pytest.mark.gpu
+def test_solve_batch_float32_input_matches_fp64():
+    """A float32 (count, n, n) batch goes to qb_solve_batch_f32 without an fp64 copy; results are those of the
+    same batch converted to fp64 (config C: fp32-valued U[-1, 1) entries), including a lower-triangular
+    entry that the native fold adds into the upper triangle."""
+    import paper_2310_19373_b200 as qb
+    from paper_2310_19373_b200 import instances
+
+    b64 = instances.config_batch(300, 16)
+    b32 = b64.astype(np.float32)
+    assert np.array_equal(b32.astype(np.float64), b64)  # config C values are float32-representable
+    b32[7, 5, 2] = np.float32(0.3)  # below the diagonal: folded into (2, 5)
+    b64 = b32.astype(np.float64)
+    m32, v32 = qb.solve_batch(b32, as_arrays=True)
+    m64, v64 = qb.solve_batch(b64, as_arrays=True)
+    assert np.array_equal(m32, m64) and np.array_equal(v32, v64)
+    sol = qb.solve_incremental(qb.QuboInstance(b64[7]))
+    assert np.array_equal(m32[7], sol.minimizer) and v32[7] == sol.value
+    bad = b32.copy()
+    bad[3, 1, 1] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        qb.solve_batch(bad, as_arrays=True)
