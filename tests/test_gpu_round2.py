@@ -212,3 +212,19 @@ def test_first_minimiser_in_gray_order_where_the_reference_drifts():
         sol = qb.solve_parallel(inst, qb.SolveConfig(threads=4, fixed_bits=2))
         assert (_bits(sol), sol.value) == (case["results"]["2"]["contract_bits"], case["results"]["2"]["contract_value"])
     assert differ == fx["drift_decided_results"]
+
+
+# ------------------------------------------------------------------ randomised soaks against the oracle (short forms)
+@pytest.mark.parametrize("tool,args", [("fuzz_oracle.py", ["40", "5", "12", "22"]), ("fuzz_batch.py", ["8", "11"])])
+def test_randomised_soak_against_oracle_and_enumeration(tool, args):
+    """Short runs of tools/fuzz_oracle.py (every kernel variant and AUTO against the oracle and, for n <= 20, a full
+    enumeration of evaluate()) and tools/fuzz_batch.py (batch kernels, float32 input, all-minimisers).  The long runs
+    are recorded in profiles/r14_fuzz_*.log.  Exit status 1 = an answer the GPU should not have returned."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    run = subprocess.run([sys.executable, os.path.join(root, "tools", tool), *args], capture_output=True, text=True,
+                         timeout=900)
+    assert run.returncode == 0, run.stdout[-3000:] + run.stderr[-3000:]
+    assert "0 mismatches (BUG)" in run.stdout
