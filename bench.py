@@ -18,6 +18,8 @@ e2e    = the same metric through the public API (solve_incremental at N=1,
 Timing hygiene: W warm-up steps; a 256 MiB L2 flush between timed steps; nvidia-smi clocks
 sampled during the timed region.  cpu_baseline: the oracle port of the reference's solver
 (oracle/, C, all host threads) on a bounded sample of the same workload, rank 0 at N=1.
+--impl reference: the unmodified reference package (baseline/_ref, numba kernels) on all host
+cores when it is staged, else the oracle port; each step a bounded sample (run_reference).
 """
 
 from __future__ import annotations
@@ -320,6 +322,50 @@ def cpu_sample(coeffs, seconds: float):
             "seconds": dt}
 
 
+def numba_reference_sample(coeffs, seconds: float):
+    """The UNMODIFIED reference package (baseline/_ref, staged by tools/stage_reference.sh; numba kernels) on the
+    same kind of sample as cpu_sample: whole 2^26-state subspaces through its own ``solve_subspace`` on a thread pool
+    of all host cores, which is what its ``solve_parallel`` runs (solver.py:214-222).  Informational: the arm's value
+    stays the C port.  None / {"unavailable": ...} when the staged reference or numba is missing."""
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "qubrute")):
+        return {"unavailable": "baseline/_ref/qubrute not staged (tools/stage_reference.sh)"}
+    sys.path.insert(0, ref)
+    try:
+        import qubrute as ref_qb
+        from concurrent.futures import ThreadPoolExecutor
+    except Exception as exc:  # numba missing or broken
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    finally:
+        sys.path.remove(ref)
+    n = coeffs.shape[0]
+    threads = os.cpu_count() or 1
+    m = max(0, n - 26)
+    inst = ref_qb.QuboInstance(coeffs)
+    ref_qb.solve_incremental(ref_qb.random_instance(6, 0))  # JIT warm-up, as the reference's own bench does (cli.py:78-83)
+    t0 = time.perf_counter()
+    ref_qb.solve_subspace(inst, ref_qb.SubspaceSpec(m=m, suffix=0))
+    one = time.perf_counter() - t0
+    count = min(1 << m, threads * max(1, int(seconds / max(one, 1e-3))))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        list(pool.map(lambda sfx: ref_qb.solve_subspace(inst, ref_qb.SubspaceSpec(m=m, suffix=sfx)), range(count)))
+    dt = time.perf_counter() - t0
+    states = count * (1 << (n - m))
+    return {"value": states / dt, "unit": "states/s", "cores": threads, "kind": "reference",
+            "sample": f"{count} of {1 << m} m={m} subspaces ({states:.3g} states, {dt:.1f} s) through the unmodified "
+                      f"reference's solve_subspace (numba {_numba_version()}) on a pool of {threads} threads",
+            "seconds": dt}
+
+
+def _numba_version() -> str:
+    try:
+        import numba
+        return numba.__version__
+    except Exception:
+        return "?"
+
+
 def extra_configs(qb, _lib, instances, reps: int = 5):
     """Informational per-config throughput (rank 0, N=1): BASELINE configs A-D besides the
     headline E.  kernel = device time of the solve launches (library CUDA events); e2e = the
@@ -366,7 +412,9 @@ def extra_configs(qb, _lib, instances, reps: int = 5):
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU solver (oracle port) on the box's host cores."""
+    """--impl reference: the reference's CPU solver on the box's host cores.  When the unmodified reference is staged
+    (baseline/_ref, numba importable) every step times IT (kind "reference") and one sample of the oracle port is
+    reported beside it; otherwise the steps time the port (kind "port")."""
     from paper_2310_19373_b200 import instances
 
     if rank != 0:
@@ -374,29 +422,45 @@ def run_reference(args, world, rank):
     coeffs = instances.config_coeffs(args.config, 0)
     n = coeffs.shape[0]
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    try:
+        probe = numba_reference_sample(coeffs, 0.5)  # also the JIT warm-up
+    except Exception as exc:
+        probe = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    real = "value" in probe
+    sample = (lambda sec: numba_reference_sample(coeffs, sec)) if real else (lambda sec: cpu_sample(coeffs, sec))
     for _ in range(args.warmup):
-        cpu_sample(coeffs, 0.5)
+        sample(0.5)
     vals, secs = [], []
     for _ in range(args.steps):
-        s = cpu_sample(coeffs, per_step)
+        s = sample(per_step)
         vals.append(s["value"])
         secs.append(s["seconds"])
     value = statistics.median(vals)
+    what = ("the unmodified reference package (baseline/_ref, numba kernels; solve_subspace on a thread pool, as its "
+            "solve_parallel runs)" if real else "oracle/gray_oracle.c (the reference's solve_parallel restated in C)")
     line = {
         "impl": "reference", "metric": "QUBO states evaluated/sec (2^n / solve time)", "value": value,
         "unit": "states/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, bench_seed(40,0))",
         "extrapolated": True,
-        "extrapolation": f"each step times a bounded sample ({s['sample']}, median {statistics.median(secs):.1f} s); "
+        "extrapolation": f"each step times a bounded sample of {what} ({s['sample']}, median "
+                         f"{statistics.median(secs):.1f} s); "
                          f"value = sampled states/s (subspaces are equal-sized, so the rate is unbiased); "
                          "ms_per_step = the timed sample; full_solve_ms_extrapolated = 2^n states at that rate",
         "full_solve_ms_extrapolated": 1e3 * 2 ** n / value,
         "config": bench_config(args.config, n),
-        "cpu_baseline": {"value": value, "unit": "states/s", "cores": s["cores"], "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "states/s", "cores": s["cores"], "kind": s["kind"],
                          "sample": s["sample"]},
         "e2e": {"value": value, "unit": "states/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if real:
+        # the C port beside the real reference, one sample (the GPU arm's cpu_baseline uses the port)
+        port = cpu_sample(coeffs, min(per_step, 10.0))
+        line["oracle_port"] = {k: port[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["oracle_port"]["port_over_reference"] = port["value"] / value
+    else:
+        line["reference_numba"] = probe
     print(json.dumps(line), flush=True)
 
 
