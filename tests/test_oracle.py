@@ -160,3 +160,28 @@ def test_oracle_reproduces_drift_decided_reference_answers():
             assert want["reference_value"] == want["contract_value"]
             decided += bits != want["contract_bits"]
     assert decided == fx["drift_decided_results"]
+
+
+def test_enumeration_checker_agrees_with_oracle_where_fp64_is_exact():
+    """tools/fuzz_common.truth (full enumeration of evaluate() + the tie key: the checker of this library's own
+    contract in the soaks and in test_gpu_round2) against the oracle on integer, half-integer and fp32-valued
+    instances, where fp64 running sums are exact and the reference therefore returns the first minimiser."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_common as F
+
+    rng = np.random.default_rng(31)
+    done = 0
+    while done < 60:
+        n = int(rng.integers(3, 14))
+        fam, c = F.make(rng, n)
+        if fam not in (1, 2, 3, 10, 11):
+            continue
+        m = min(int(rng.choice([0, 2, 5])), n - 2)
+        assert F.truth(c, n, m, None) == O.solve_subspaces(c, m)[:2], (fam, n, m)
+        if m:
+            s = int(rng.integers(0, 1 << m))
+            assert F.truth(c, n, m, s) == O.solve_subspaces(c, m, s, s + 1)[:2], (fam, n, m, s)
+        done += 1
