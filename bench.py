@@ -504,11 +504,12 @@ def main():
     if args.shared_device:
         os.environ["QB_SHARED_DEVICE"] = "1"
         os.environ.setdefault("QB_DIST_BACKEND", "gloo")
+    if args.impl == "reference":
+        # CPU only, rank 0 alone: no process group, no collective (the other ranks of a torchrun launch exit 0)
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
     world, rank, local = dist_setup(args.gpus)
     os.environ["QB_DEVICE"] = str(local)  # the library's default device follows the rank -> GPU map
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-        return
 
     import numpy as np
     import torch
